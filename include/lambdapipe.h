@@ -1,0 +1,111 @@
+/* lambdapipe — C ABI of the B200-native λScale scaling hot path.
+ *
+ * The reference (blockcast, pkg/src/blockcast/) has no native layer: its data
+ * plane is a cost formula (simengine.py:95-103) and an event that adds block
+ * ids to a set (simengine.py:628-644).  This ABI is the bottom layer the
+ * reference's planner would call to move real bytes and run real tokens; the
+ * Python package paper_2502_09922_b200 wraps it with the reference's own
+ * function names (INTEGRATION.md shows the ctypes binding a blockcast
+ * maintainer would add).
+ *
+ * Conventions
+ *   - every entry point returns 0 on success, <0 on failure; lp_last_error()
+ *     returns a thread-local message for the last failure on this thread;
+ *   - buffers are borrowed (device pointers in this process: local, CUDA-IPC
+ *     mapped peers, or device aliases of registered pinned host memory);
+ *     nothing allocated by the caller is freed by the library;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *   - work is asynchronous on the given stream unless stated otherwise.
+ */
+#ifndef LAMBDAPIPE_H
+#define LAMBDAPIPE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- library / device plumbing ----------------------------------------- */
+int         lp_version(void);
+const char* lp_last_error(void);
+int lp_device_count(int* n);
+int lp_set_device(int dev);
+int lp_sync_device(int dev);
+/* cudaDeviceEnablePeerAccess(dev -> peer); already-enabled is not an error */
+int lp_enable_peer(int dev, int peer);
+int lp_malloc(int dev, int64_t bytes, void** out);
+int lp_free(int dev, void* ptr);
+int lp_memset(void* dst, int value, int64_t bytes, void* stream);
+int lp_memcpy(void* dst, const void* src, int64_t bytes, void* stream); /* cudaMemcpyDefault */
+/* CUDA IPC: 64-byte opaque handle for a device allocation from lp_malloc */
+int lp_ipc_get(void* dev_ptr, void* handle64);
+int lp_ipc_open(int dev, const void* handle64, void** out);
+int lp_ipc_close(void* ptr);
+/* pin + map host memory (e.g. a shared-memory segment); returns device alias */
+int lp_host_register(void* host, int64_t bytes, void** dev_alias);
+int lp_host_unregister(void* host);
+int lp_stream_create(int dev, void** stream);
+int lp_stream_destroy(void* stream);
+int lp_stream_sync(void* stream);
+int lp_event_create(void** ev);
+int lp_event_destroy(void* ev);
+int lp_event_record(void* ev, void* stream);
+int lp_event_elapsed_ms(void* start, void* end, float* ms);
+
+/* ---- synthetic packed image + per-block checksums ----------------------
+ * Replaces the reference's "bytes never move" block model
+ * (multicast.py:153-173 block sizes; modelmgr.py:238-259 packing): the image
+ * holds real tensors.  Tensor t occupies [off[t], off[t]+numel[t]*2) and is
+ * filled with bf16 values from the counter-based generator (oracle/dataplane.c
+ * lp_ref_fill restates it): kind 0 = random in [-2^scale_exp, 2^scale_exp),
+ * kind 1 = ones, kind 2 = zeros. */
+int lp_fill_tensors(void* base, int n_tensors, const int64_t* off, const int64_t* numel,
+                    const int32_t* kind, const int32_t* scale_exp, uint64_t seed, void* stream);
+/* out[i] = sum_w mix64(word_w ^ w*K) over 8-byte words of block i (wraps mod 2^64) */
+int lp_block_checksums(const void* base, int n_blocks, const int64_t* off, const int64_t* len,
+                       uint64_t* out_host, void* stream);
+
+/* ---- λPipe multicast engine ----------------------------------------------
+ * Executes a reference schedule (schedule_to_lines, multicast.py:546-551) as
+ * a dataflow: each transfer (step, sender, receiver, block) becomes a push of
+ * the block's tiles from sender to receiver over NVLink (in-kernel 16-byte
+ * peer stores), or, when the sender is a HOST node, a pull of the tiles by
+ * the receiver over PCIe from mapped pinned memory.  A relay forwards tile t
+ * of a block as soon as tile t landed (chunk cut-through).  The transfer set,
+ * each sender's send order and each receiver's delivered bytes are exactly
+ * the schedule's (replaces simengine.py:594-596 + :628-644). */
+typedef struct lp_mc lp_mc;
+#define LP_NODE_GPU  0
+#define LP_NODE_HOST 1
+int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_off,
+                 const int64_t* block_len, int64_t tile_bytes);
+int lp_mc_destroy(lp_mc* mc);
+/* bytes of the per-node signal area (tile flags, block counters, arrivals) */
+int lp_mc_signal_bytes(const lp_mc* mc, int64_t* bytes);
+/* image/signals: device-visible pointers in this process; host nodes pass
+ * signals = NULL.  ready_host (optional) = device alias of pinned host words,
+ * one u32 per block, set to the epoch when the block is complete. */
+int lp_mc_set_node(lp_mc* mc, int node, int kind, void* image, void* signals, void* ready_host);
+/* xfers = n_xfers x 4 int32 rows (step, sender, receiver, block), any order;
+ * sources hold every block before step 0 (multicast.py:111-124). */
+int lp_mc_set_schedule(lp_mc* mc, const int32_t* xfers, int n_xfers,
+                       const int32_t* sources, int n_sources);
+/* run every transfer whose executor is in exec_nodes (GPU senders push,
+ * host-sourced transfers are pulled by their receiver); each exec node's
+ * CTAs also wait until all its incoming tiles of this epoch landed. */
+int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch,
+              int push_ctas, int pull_ctas, void* stream);
+/* synchronise `stream`; code = 1 (and return -3) if a flag wait timed out */
+int lp_mc_status(lp_mc* mc, void* stream, int* code);
+/* zero a node's signal area (call on every node, then barrier, before epoch 1) */
+int lp_mc_reset_signals(lp_mc* mc, int node, void* stream);
+/* synchronous: per-block arrival globaltimer (ns) at `node` for the last run,
+ * and the executed-transfer count per node (sanity) */
+int lp_mc_arrivals(lp_mc* mc, int node, uint64_t* out_ns);
+int lp_mc_block_complete(lp_mc* mc, int node, uint32_t epoch, int32_t* out_flags);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAMBDAPIPE_H */

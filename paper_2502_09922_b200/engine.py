@@ -1,0 +1,349 @@
+"""Host side of the λPipe multicast engine (wraps ``lp_mc_*`` of the C ABI).
+
+:class:`MulticastEngine` owns one ``lp_mc`` handle: the block table of a
+packed image, a node table (device-visible image + signal area per node) and a
+compiled schedule.  :class:`Cluster` is the set of node images one process
+can address:
+
+* ``Cluster.local(...)``   — every node's image on ONE GPU, executed by one
+  kernel launch (test / single-GPU emulation; the guide's rule for fewer GPUs
+  than ranks);
+* ``Cluster.distributed(...)`` — one process per GPU under torchrun; images
+  are exchanged as CUDA-IPC handles so each rank pushes straight into its
+  peers' HBM over NVLink;
+* an optional HOST node: pinned (page-locked, device-mapped) host memory that
+  receivers pull from over PCIe (config C3).  In the distributed case it lives
+  in a POSIX shared-memory segment that every rank maps and registers.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import mmap
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import InvalidArgumentError, NativeError
+from .image import fill_args
+
+LP_NODE_GPU, LP_NODE_HOST = 0, 1
+DEFAULT_TILE = 512 * 1024
+
+
+class _CudaArray:
+    """Minimal ``__cuda_array_interface__`` view of a raw device pointer."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def device_view(ptr: int, nbytes: int, device: int, dtype=None, shape=None):
+    """A torch tensor aliasing ``nbytes`` of device memory at ``ptr`` (no copy)."""
+    import torch
+    dtype = dtype or torch.uint8
+    base = torch.int16 if dtype == torch.bfloat16 else dtype
+    typestr = {torch.uint8: "|u1", torch.int16: "<i2", torch.float16: "<f2", torch.float32: "<f4",
+               torch.int32: "<i4", torch.int64: "<i8"}[base]
+    n = nbytes // torch.empty((), dtype=base).element_size()
+    with torch.cuda.device(device):
+        t = torch.as_tensor(_CudaArray(ptr, (n,), typestr), device=f"cuda:{device}")
+    if dtype == torch.bfloat16:
+        t = t.view(torch.bfloat16)
+    return t.view(shape) if shape is not None else t
+
+
+class MulticastEngine:
+    """One compiled λPipe multicast over a fixed block table."""
+
+    def __init__(self, n_nodes: int, block_offsets, block_lengths, tile_bytes: int = DEFAULT_TILE):
+        lib = N.lib()
+        self.n_nodes = n_nodes
+        self.n_blocks = len(block_offsets)
+        self.block_offsets = list(block_offsets)
+        self.block_lengths = list(block_lengths)
+        self.tile_bytes = tile_bytes
+        h = C.c_void_p()
+        N.check(lib.lp_mc_create(C.byref(h), n_nodes, self.n_blocks, N.i64_array(block_offsets),
+                                 N.i64_array(block_lengths), tile_bytes), "lp_mc_create")
+        self._h = h
+        sb = C.c_int64()
+        N.check(lib.lp_mc_signal_bytes(h, C.byref(sb)), "lp_mc_signal_bytes")
+        self.signal_bytes = sb.value
+
+    def close(self):
+        if self._h:
+            N.lib().lp_mc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_node(self, node: int, kind: int, image: int, signals: int = 0, ready: int = 0):
+        N.call("lp_mc_set_node", self._h, node, kind, C.c_void_p(image), C.c_void_p(signals or None),
+               C.c_void_p(ready or None))
+
+    def set_schedule(self, rows, sources):
+        flat = [int(v) for r in rows for v in r]
+        arr = N.i32_array(flat) if flat else (C.c_int32 * 1)()
+        N.call("lp_mc_set_schedule", self._h, arr, len(rows), N.i32_array(list(sources)), len(sources))
+
+    def reset_signals(self, node: int, stream: int = 0):
+        N.call("lp_mc_reset_signals", self._h, node, C.c_void_p(stream or None))
+
+    def run(self, exec_nodes, epoch: int, push_ctas: int, pull_ctas: int, stream: int = 0):
+        N.call("lp_mc_run", self._h, N.i32_array(list(exec_nodes)), len(exec_nodes), epoch,
+               push_ctas, pull_ctas, C.c_void_p(stream or None))
+
+    def status(self, stream: int = 0) -> None:
+        code = C.c_int()
+        N.call("lp_mc_status", self._h, C.c_void_p(stream or None), C.byref(code))
+
+    def arrivals_ns(self, node: int) -> list:
+        out = (C.c_uint64 * self.n_blocks)()
+        N.call("lp_mc_arrivals", self._h, node, out)
+        return list(out)
+
+    def complete(self, node: int, epoch: int) -> list:
+        out = (C.c_int32 * self.n_blocks)()
+        N.call("lp_mc_block_complete", self._h, node, epoch, out)
+        return [bool(x) for x in out]
+
+
+def schedule_rows(schedule) -> list:
+    """(step, sender, receiver, block) rows of a MulticastSchedule or its lines."""
+    if isinstance(schedule, (list, tuple)) and schedule and isinstance(schedule[0], str):
+        return [tuple(int(x) for x in ln.split(",")) for ln in schedule]
+    return [(t.step, t.sender, t.receiver, t.block_id) for row in schedule.steps for t in row]
+
+
+@dataclass
+class NodeBuffer:
+    node: int
+    kind: int
+    device: int              # CUDA device holding it (-1 for host)
+    image: int               # device-visible pointer in this process
+    signals: int = 0
+    owned: list = field(default_factory=list)   # (kind, ptr) to free
+
+
+class HostImage:
+    """Page-locked, device-mapped host copy of a packed image (a HOST node).
+
+    ``shm_name`` backs it with a POSIX shared-memory file so every rank of a
+    torchrun job maps the same pages (``/dev/shm``); otherwise anonymous.
+    """
+
+    def __init__(self, nbytes: int, shm_name: str | None = None, create: bool = True):
+        self.nbytes = nbytes
+        self.shm_path = None
+        if shm_name:
+            self.shm_path = f"/dev/shm/{shm_name}"
+            flags = os.O_RDWR | (os.O_CREAT if create else 0)
+            fd = os.open(self.shm_path, flags, 0o600)
+            if create:
+                os.ftruncate(fd, nbytes)
+            self._mm = mmap.mmap(fd, nbytes, mmap.MAP_SHARED, mmap.PROT_READ | mmap.PROT_WRITE)
+            os.close(fd)
+        else:
+            self._mm = mmap.mmap(-1, nbytes, mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS,
+                                 mmap.PROT_READ | mmap.PROT_WRITE)
+        self.array = np.frombuffer(self._mm, dtype=np.uint8)
+        self.host_ptr = self.array.ctypes.data
+        alias = C.c_void_p()
+        N.call("lp_host_register", C.c_void_p(self.host_ptr), nbytes, C.byref(alias))
+        self.device_ptr = alias.value
+
+    def close(self, unlink: bool = False):
+        if self.device_ptr:
+            N.lib().lp_host_unregister(C.c_void_p(self.host_ptr))
+            self.device_ptr = 0
+        self.array = None
+        try:
+            self._mm.close()
+        except BufferError:
+            pass
+        if unlink and self.shm_path and os.path.exists(self.shm_path):
+            os.unlink(self.shm_path)
+
+
+def dev_malloc(device: int, nbytes: int) -> int:
+    p = C.c_void_p()
+    N.call("lp_malloc", device, nbytes, C.byref(p))
+    return p.value
+
+
+def dev_free(device: int, ptr: int):
+    N.call("lp_free", device, C.c_void_p(ptr))
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = (C.c_char * 64)()
+    N.call("lp_ipc_get", C.c_void_p(ptr), buf)
+    return bytes(buf)
+
+
+def ipc_open(device: int, handle: bytes) -> int:
+    p = C.c_void_p()
+    buf = (C.c_char * 64).from_buffer_copy(handle)
+    N.call("lp_ipc_open", device, buf, C.byref(p))
+    return p.value
+
+
+def fill_image(device_ptr: int, layout, seed: int, stream: int = 0):
+    """Write the synthetic weights of ``layout`` into an image on the device."""
+    off, numel, kind, sexp, _ = fill_args(layout)
+    n = len(off)
+    N.call("lp_fill_tensors", C.c_void_p(device_ptr), n, N.i64_array(off), N.i64_array(numel),
+           N.i32_array(kind), N.i32_array(sexp), C.c_uint64(seed), C.c_void_p(stream or None))
+
+
+def block_checksums(device_ptr: int, offsets, lengths, stream: int = 0) -> list:
+    out = (C.c_uint64 * len(offsets))()
+    N.call("lp_block_checksums", C.c_void_p(device_ptr), len(offsets), N.i64_array(offsets),
+           N.i64_array(lengths), out, C.c_void_p(stream or None))
+    return list(out)
+
+
+class Cluster:
+    """Node images addressable from this process + the engine that moves them."""
+
+    def __init__(self, engine: MulticastEngine, nodes: list, exec_nodes: list, rank: int = 0,
+                 world: int = 1, host: HostImage | None = None):
+        self.engine = engine
+        self.nodes = nodes
+        self.exec_nodes = exec_nodes
+        self.rank, self.world = rank, world
+        self.host = host
+        self.epoch = 0
+
+    # -- construction ---------------------------------------------------------
+
+    @classmethod
+    def local(cls, n_gpu_nodes: int, block_offsets, block_lengths, image_bytes: int, device: int = 0,
+              host_node: bool = False, tile_bytes: int = DEFAULT_TILE):
+        """All GPU nodes on one device (node ids 1.. if a host node 0 exists)."""
+        n_nodes = n_gpu_nodes + (1 if host_node else 0)
+        N.call("lp_set_device", device)
+        eng = MulticastEngine(n_nodes, block_offsets, block_lengths, tile_bytes)
+        nodes = []
+        host = None
+        first = 0
+        if host_node:
+            host = HostImage(image_bytes)
+            eng.set_node(0, LP_NODE_HOST, host.device_ptr)
+            nodes.append(NodeBuffer(0, LP_NODE_HOST, -1, host.device_ptr))
+            first = 1
+        for i in range(first, n_nodes):
+            img = dev_malloc(device, image_bytes)
+            sig = dev_malloc(device, eng.signal_bytes)
+            nb = NodeBuffer(i, LP_NODE_GPU, device, img, sig, [("dev", img), ("dev", sig)])
+            eng.set_node(i, LP_NODE_GPU, img, sig)
+            eng.reset_signals(i)
+            nodes.append(nb)
+        N.call("lp_sync_device", device)
+        exec_nodes = [nb.node for nb in nodes if nb.kind == LP_NODE_GPU]
+        return cls(eng, nodes, exec_nodes, host=host)
+
+    @classmethod
+    def distributed(cls, block_offsets, block_lengths, image_bytes: int, host_node: bool = False,
+                    tile_bytes: int = DEFAULT_TILE, shm_name: str = "lambdapipe_host_image"):
+        """One GPU node per torchrun rank (node id = rank, +1 with a host node 0)."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        device = torch.cuda.current_device()
+        off = 1 if host_node else 0
+        n_nodes = world + off
+        eng = MulticastEngine(n_nodes, block_offsets, block_lengths, tile_bytes)
+        img = dev_malloc(device, image_bytes)
+        sig = dev_malloc(device, eng.signal_bytes)
+        mine = (ipc_handle(img), ipc_handle(sig))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        nodes = []
+        host = None
+        if host_node:
+            if rank == 0:
+                host = HostImage(image_bytes, shm_name, create=True)
+            dist.barrier()
+            if rank != 0:
+                host = HostImage(image_bytes, shm_name, create=False)
+            eng.set_node(0, LP_NODE_HOST, host.device_ptr)
+            nodes.append(NodeBuffer(0, LP_NODE_HOST, -1, host.device_ptr))
+        for r in range(world):
+            node = r + off
+            if r == rank:
+                p_img, p_sig, owned = img, sig, [("dev", img), ("dev", sig)]
+            else:
+                p_img = ipc_open(device, allh[r][0])
+                p_sig = ipc_open(device, allh[r][1])
+                owned = [("ipc", p_img), ("ipc", p_sig)]
+            eng.set_node(node, LP_NODE_GPU, p_img, p_sig)
+            nodes.append(NodeBuffer(node, LP_NODE_GPU, device if r == rank else -2, p_img, p_sig, owned))
+        eng.reset_signals(rank + off)
+        N.call("lp_sync_device", device)
+        dist.barrier()
+        return cls(eng, nodes, [rank + off], rank, world, host)
+
+    def node(self, i: int) -> NodeBuffer:
+        return self.nodes[i]
+
+    def close(self):
+        for nb in self.nodes:
+            for kind, ptr in nb.owned:
+                if kind == "dev":
+                    dev_free(max(nb.device, 0), ptr)
+                else:
+                    N.lib().lp_ipc_close(C.c_void_p(ptr))
+            nb.owned = []
+        if self.host is not None:
+            self.host.close(unlink=self.rank == 0 and self.host.shm_path is not None)
+            self.host = None
+        self.engine.close()
+
+    # -- execution ------------------------------------------------------------
+
+    def set_schedule(self, schedule, sources):
+        self.engine.set_schedule(schedule_rows(schedule), sources)
+
+    def launch(self, push_ctas: int = 32, pull_ctas: int = 0, stream: int = 0, epoch: int | None = None):
+        """Launch one multicast epoch (async on ``stream``); returns the epoch."""
+        if epoch is None:
+            self.epoch += 1
+            epoch = self.epoch
+        else:
+            self.epoch = epoch
+        if push_ctas < 1:
+            raise InvalidArgumentError("push_ctas must be >= 1")
+        self.engine.run(self.exec_nodes, epoch, push_ctas, pull_ctas, stream)
+        return epoch
+
+    def wait(self, stream: int = 0):
+        try:
+            self.engine.status(stream)
+        except NativeError:
+            raise
+
+
+def load_source_image(cluster: "Cluster", node: int, layout, seed: int, device: int = 0):
+    """Materialise the synthetic weights on a source node (GPU fill; host
+    nodes get a device fill copied down over PCIe)."""
+    nb = cluster.node(node)
+    if nb.kind == LP_NODE_GPU:
+        fill_image(nb.image, layout, seed)
+        return
+    scratch = dev_malloc(device, layout.weights_bytes)
+    try:
+        fill_image(scratch, layout, seed)
+        N.call("lp_memcpy", C.c_void_p(cluster.host.host_ptr), C.c_void_p(scratch), layout.weights_bytes,
+               None)
+        N.call("lp_sync_device", device)
+    finally:
+        dev_free(device, scratch)
