@@ -91,11 +91,30 @@ int lp_mc_set_node(lp_mc* mc, int node, int kind, void* image, void* signals, vo
  * sources hold every block before step 0 (multicast.py:111-124). */
 int lp_mc_set_schedule(lp_mc* mc, const int32_t* xfers, int n_xfers,
                        const int32_t* sources, int n_sources);
-/* run every transfer whose executor is in exec_nodes (GPU senders push,
- * host-sourced transfers are pulled by their receiver); each exec node's
- * CTAs also wait until all its incoming tiles of this epoch landed. */
+/* run every transfer whose executor is in exec_nodes (see lp_mc_configure);
+ * push CTAs execute pushes, pull CTAs execute pulls; each exec node's kernel
+ * also waits until every tile pushed into it this epoch landed. */
 int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch,
               int push_ctas, int pull_ctas, void* stream);
+/* direction 0 = push: a GPU sender's CTAs store its blocks into the receiver
+ * (NVLink writes); 1 = pull (default): every transfer is executed by its
+ * receiver, which reads the sender's tiles (NVLink or PCIe reads) once the
+ * sender's flag for the tile holds the epoch.  Host-sourced transfers are
+ * always pulled.  push_mode/pull_mode pick the copy engine of each role:
+ * 0 = LDG/STG 16-byte vectors on 512 threads, 1 = TMA bulk copies
+ * (cp.async.bulk global->smem->global, one issuing thread, 12-slot smem ring
+ * of chunk_bytes).  window (>= 1; 0 keeps the current value) = how many
+ * consecutive ops of its list an LDG-role CTA may interleave when the oldest
+ * op's next tile is not ready yet. */
+int lp_mc_configure(lp_mc* mc, int direction, int push_mode, int pull_mode, int64_t chunk_bytes,
+                    int window);
+/* Copy-engine executor for one GPU node (direction 1 only): enqueue, on the
+ * node's `n_streams` streams, every transfer it receives as per-tile
+ * cuStreamWaitValue32(sender flag) -> cudaMemcpyAsync -> cuStreamWriteValue32
+ * (own flag); no SM work.  block_events (optional, n_blocks entries, NULL to
+ * skip) are recorded after each received block's last tile. */
+int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
+                 void* const* block_events);
 /* synchronise `stream`; code = 1 (and return -3) if a flag wait timed out */
 int lp_mc_status(lp_mc* mc, void* stream, int* code);
 /* zero a node's signal area (call on every node, then barrier, before epoch 1) */

@@ -46,7 +46,7 @@ def build(verbose: bool = False) -> str:
             if log:
                 sys.stderr.write(log)
     if not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcuda"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")

@@ -20,6 +20,7 @@
 // local memory).  Flags carry the run's epoch so they never need resetting.
 #include "lp_common.cuh"
 #include "../../include/lambdapipe.h"
+#include <cuda.h>
 #include <algorithm>
 #include <vector>
 
@@ -58,7 +59,10 @@ struct McParams {
   int64_t tile_bytes;
   uint64_t timeout_ns;
   uint32_t epoch;
+  uint32_t chunk_bytes;
   int push_ctas, pull_ctas, n_exec;
+  int push_mode, pull_mode;   // 0 = LDG/STG vectors, 1 = TMA bulk pipeline
+  int window;                 // ops a CTA may interleave (ldg role)
   ExecDesc exec[LP_MAX_EXEC];
 };
 
@@ -94,7 +98,233 @@ __device__ __forceinline__ void copy_tile(const char* __restrict__ s, char* __re
   for (; i < n16; i += T) lp::st16(d4 + i, lp::ld_stream16(s4 + i));
 }
 
+// ---------------------------------------------------------------------------
+// Role A: LDG/STG copy.  All 512 threads move 16-byte vectors; one thread
+// waits for the tile's flag before, and publishes the receiver's flag after.
+
+__device__ __forceinline__ void publish_tile(const NodeDev& dst, const BlockDev& bl, int block, int t,
+                                             uint32_t epoch) {
+  lp::st_release_sys(dst.flags + bl.tile_base + t, epoch);
+  const uint32_t old = lp::atom_add_release_sys(dst.counts + block, 1u);
+  if (old + 1u == epoch * (uint32_t)bl.ntiles) {
+    dst.arrival[block] = lp::globaltimer();
+    if (dst.ready) lp::st_release_sys(dst.ready + block, epoch);
+  }
+}
+
+// Ops of one role are consumed through a window of `window` consecutive ops:
+// each op's tiles are taken in order, but when the next tile of the oldest op
+// is not ready yet (its sender is a relay still receiving it), the CTA moves
+// on to the first op in the window whose next tile IS ready.  That keeps the
+// node's NVLink ingress busy instead of idling behind one slow upstream; the
+// transfer set and each op's bytes are unchanged.
+constexpr int kMaxWindow = 8;
+
+__device__ void ldg_role(const McParams& p, int ob, int oe, int lane, int lanes, uint64_t t0, int* s_ok) {
+  const uint32_t epoch = p.epoch;
+  const int W = p.window < 1 ? 1 : (p.window > kMaxWindow ? kMaxWindow : p.window);
+  __shared__ int cur[kMaxWindow];
+  __shared__ int s_base, s_pick, s_tile;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < kMaxWindow; ++w) cur[w] = lane;
+    s_base = ob;
+  }
+  __syncthreads();
+  while (true) {
+    if (threadIdx.x == 0) {
+      int base = s_base;
+      while (base < oe && cur[0] >= p.blocks[p.ops[base].block].ntiles) {
+        for (int w = 0; w + 1 < W; ++w) cur[w] = cur[w + 1];
+        cur[W - 1] = lane;
+        ++base;
+      }
+      s_base = base;
+      int pick = -1;
+      for (int w = 0; w < W && base + w < oe; ++w) {
+        const OpDev op = p.ops[base + w];
+        const BlockDev bl = p.blocks[op.block];
+        if (cur[w] >= bl.ntiles) continue;
+        if (!op.wait || lp::ld_acquire_sys(p.nodes[op.src].flags + bl.tile_base + cur[w]) == epoch) {
+          pick = w;
+          break;
+        }
+      }
+      if (pick < 0 && base < oe) {  // nothing ready: block on the oldest op's next tile
+        for (int w = 0; w < W && base + w < oe; ++w) {
+          const OpDev op = p.ops[base + w];
+          const BlockDev bl = p.blocks[op.block];
+          if (cur[w] >= bl.ntiles) continue;
+          if (!wait_flag(p.nodes[op.src].flags + bl.tile_base + cur[w], epoch, t0, p.timeout_ns, p.err))
+            *s_ok = 0;
+          pick = w;
+          break;
+        }
+      }
+      s_pick = pick < 0 ? -1 : base + pick;
+      s_tile = pick < 0 ? 0 : cur[pick];
+      if (pick >= 0) cur[pick] += lanes;
+    }
+    __syncthreads();
+    const int oi = s_pick;
+    const int t = s_tile;
+    if (oi < 0 || !*s_ok) return;
+    const OpDev op = p.ops[oi];
+    const BlockDev bl = p.blocks[op.block];
+    const NodeDev src = p.nodes[op.src];
+    const NodeDev dst = p.nodes[op.dst];
+    const int64_t lo = (int64_t)t * p.tile_bytes;
+    const int64_t n = min(p.tile_bytes, bl.len - lo);
+    copy_tile(src.image + bl.off + lo, dst.image + bl.off + lo, n);
+    __syncthreads();  // every thread's stores of this tile precede the flag
+    if (threadIdx.x == 0) {
+      lp::fence_sys();
+      publish_tile(dst, bl, op.block, t, epoch);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Role B: TMA bulk-copy pipeline driven by ONE thread.  Tiles are cut into
+// chunks; chunk q is loaded HBM(or host)->smem ring slot q % S with
+// cp.async.bulk (mbarrier completion) and stored smem->destination with a
+// bulk_group store (the destination is the peer's image over NVLink).  Loads
+// run LA = 3 chunks ahead of stores, leaving S - LA slots to stores in flight
+// (a slot is reusable once its store has READ it, which over NVLink takes
+// about the write latency, so in-flight stores set the per-CTA rate); a tile's flag is published once its
+// last store group completed (bulk wait_group), a few groups after issue, so
+// the pipeline never drains between tiles.
+
+constexpr int kStages = 12;
+constexpr int kLookaheadPush = 3;   // local HBM reads: short latency, many stores in flight
+constexpr int kLookaheadPull = 9;   // remote NVLink / PCIe reads: long latency, local stores
+constexpr int kPendTiles = 16;
+
+struct ChunkDesc {
+  const char* src;
+  char* dst;
+  uint32_t bytes;
+  int32_t last;      // last chunk of its tile
+  int32_t op;        // op index (for publishing)
+  int32_t tile;
+};
+
+struct TileGen {  // walks (op, my tiles, chunks) in order
+  int oi, oe, t, lane, lanes;
+  int64_t c;         // byte offset within the tile
+};
+
+__device__ void tma_role(const McParams& p, int ob, int oe, int lane, int lanes, uint64_t t0, int* s_ok,
+                         char* ring, uint64_t* bars, const int lookahead) {
+  if (threadIdx.x != 0) return;
+  const uint32_t epoch = p.epoch;
+  const uint32_t chunk = p.chunk_bytes;
+  ChunkDesc desc[kStages];
+  int pend_op[kPendTiles], pend_tile[kPendTiles];
+  int64_t pend_group[kPendTiles];
+  int pend_head = 0, pend_tail = 0;
+  int64_t q_load = 0, q_store = 0;
+
+  TileGen g{ob, oe, lane, lane, lanes, 0};
+  // skip ops with no tile for this lane
+  auto settle = [&]() {
+    while (g.oi < g.oe && g.t >= p.blocks[p.ops[g.oi].block].ntiles) {
+      ++g.oi;
+      g.t = g.lane;
+      g.c = 0;
+    }
+  };
+  settle();
+
+  auto publish_ready = [&](bool force) {
+    while (pend_head != pend_tail) {
+      const int i = pend_head % kPendTiles;
+      const int64_t after = q_store - 1 - pend_group[i];  // groups issued after the tile's last one
+      if (!force && after < kStages - 1) break;
+      lp::bulk_wait_n((int)(after < 0 ? 0 : after));
+      lp::fence_proxy_async_global();
+      lp::fence_sys();
+      const OpDev op = p.ops[pend_op[i]];
+      publish_tile(p.nodes[op.dst], p.blocks[op.block], op.block, pend_tile[i], epoch);
+      ++pend_head;
+    }
+  };
+
+  auto store_one = [&]() {
+    const int slot = (int)(q_store % kStages);
+    lp::mbar_wait(&bars[slot], (uint32_t)((q_store / kStages) & 1));
+    const ChunkDesc d = desc[slot];
+    lp::bulk_s2g(d.dst, ring + (size_t)slot * chunk, d.bytes);
+    lp::bulk_commit();
+    if (d.last) {
+      if (pend_tail - pend_head == kPendTiles) publish_ready(true);
+      const int i = pend_tail % kPendTiles;
+      pend_op[i] = d.op;
+      pend_tile[i] = d.tile;
+      pend_group[i] = q_store;
+      ++pend_tail;
+    }
+    ++q_store;
+    publish_ready(false);
+  };
+
+  while (true) {
+    const bool have_next = g.oi < g.oe;
+    if (!have_next && q_store == q_load) break;
+    if (have_next && q_load - q_store < lookahead) {
+      const OpDev op = p.ops[g.oi];
+      const BlockDev bl = p.blocks[op.block];
+      const NodeDev src = p.nodes[op.src];
+      const NodeDev dst = p.nodes[op.dst];
+      if (g.c == 0 && op.wait) {
+        const uint32_t* f = src.flags + bl.tile_base + g.t;
+        if (lp::ld_acquire_sys(f) != epoch) {
+          if (q_store < q_load) {  // keep the pipe moving while the tile is in flight upstream
+            store_one();
+            continue;
+          }
+          publish_ready(true);
+          if (!wait_flag(f, epoch, t0, p.timeout_ns, p.err)) {
+            *s_ok = 0;
+            lp::bulk_wait<0>();
+            return;
+          }
+        }
+        lp::fence_proxy_async_global();  // order the acquire before async-proxy reads
+      }
+      const int64_t tlo = (int64_t)g.t * p.tile_bytes;
+      const int64_t tlen = min(p.tile_bytes, bl.len - tlo);
+      const uint32_t nb = (uint32_t)min((int64_t)chunk, tlen - g.c);
+      const int slot = (int)(q_load % kStages);
+      if (q_load >= kStages) lp::bulk_wait_read_n((int)(q_store - 1 - (q_load - kStages)));
+      ChunkDesc d;
+      d.src = src.image + bl.off + tlo + g.c;
+      d.dst = dst.image + bl.off + tlo + g.c;
+      d.bytes = nb;
+      d.last = (g.c + nb >= tlen) ? 1 : 0;
+      d.op = g.oi;
+      d.tile = g.t;
+      desc[slot] = d;
+      lp::mbar_expect_tx(&bars[slot], nb);
+      lp::bulk_g2s(ring + (size_t)slot * chunk, d.src, nb, &bars[slot]);
+      ++q_load;
+      g.c += nb;
+      if (g.c >= tlen) {
+        g.c = 0;
+        g.t += g.lanes;
+        settle();
+      }
+    } else {
+      store_one();
+    }
+  }
+  lp::bulk_wait<0>();
+  publish_ready(true);
+}
+
 __global__ void __launch_bounds__(LP_MC_THREADS) mc_kernel(const McParams p) {
+  extern __shared__ __align__(128) char ring[];
+  __shared__ uint64_t bars[kStages];
+  __shared__ int s_ok;
   const int per = p.push_ctas + p.pull_ctas;
   const int e = blockIdx.x / per;
   const int local = blockIdx.x % per;
@@ -104,51 +334,29 @@ __global__ void __launch_bounds__(LP_MC_THREADS) mc_kernel(const McParams p) {
   const int lanes = pusher ? p.push_ctas : p.pull_ctas;
   const int ob = pusher ? ex.push_b : ex.pull_b;
   const int oe = pusher ? ex.push_e : ex.pull_e;
-  const uint32_t epoch = p.epoch;
-  __shared__ int s_ok;
+  const bool tma = pusher ? (p.push_mode == 1) : (p.pull_mode == 1);
   uint64_t t0 = 0;
   if (threadIdx.x == 0) {
     t0 = lp::globaltimer();
     s_ok = 1;
-  }
-
-  for (int oi = ob; oi < oe; ++oi) {
-    const OpDev op = p.ops[oi];
-    const BlockDev bl = p.blocks[op.block];
-    const NodeDev src = p.nodes[op.src];
-    const NodeDev dst = p.nodes[op.dst];
-    for (int t = lane; t < bl.ntiles; t += lanes) {
-      const int64_t lo = (int64_t)t * p.tile_bytes;
-      const int64_t n = min(p.tile_bytes, bl.len - lo);
-      if (op.wait) {
-        if (threadIdx.x == 0 && !wait_flag(src.flags + bl.tile_base + t, epoch, t0, p.timeout_ns, p.err))
-          s_ok = 0;
-        __syncthreads();
-        if (!s_ok) return;
-      }
-      copy_tile(src.image + bl.off + lo, dst.image + bl.off + lo, n);
-      __syncthreads();  // every thread's stores of this tile precede the flag
-      if (threadIdx.x == 0) {
-        lp::fence_sys();
-        lp::st_release_sys(dst.flags + bl.tile_base + t, epoch);
-        const uint32_t old = lp::atom_add_release_sys(dst.counts + op.block, 1u);
-        if (old + 1u == epoch * (uint32_t)bl.ntiles) {
-          dst.arrival[op.block] = lp::globaltimer();
-          if (dst.ready) lp::st_release_sys(dst.ready + op.block, epoch);
-        }
-      }
+    if (tma) {
+      for (int i = 0; i < kStages; ++i) lp::mbar_init(&bars[i], 1);
+      lp::fence_mbar_init();
     }
   }
+  __syncthreads();
+  if (tma)
+    tma_role(p, ob, oe, lane, lanes, t0, &s_ok, ring, bars, pusher ? kLookaheadPush : kLookaheadPull);
+  else
+    ldg_role(p, ob, oe, lane, lanes, t0, &s_ok);
 
   // the node is complete when every tile it receives this epoch has landed
-  if (pusher) {
+  if (pusher && threadIdx.x == 0 && s_ok) {
     const NodeDev me = p.nodes[ex.node];
     for (int r = ex.recv_b; r < ex.recv_e; ++r) {
       const BlockDev bl = p.blocks[p.recv_blocks[r]];
       for (int t = lane; t < bl.ntiles; t += lanes) {
-        if (threadIdx.x == 0 && s_ok &&
-            !wait_flag(me.flags + bl.tile_base + t, epoch, t0, p.timeout_ns, p.err))
-          s_ok = 0;
+        if (!wait_flag(me.flags + bl.tile_base + t, p.epoch, t0, p.timeout_ns, p.err)) return;
       }
     }
   }
@@ -168,6 +376,7 @@ struct lp_mc {
   bool dirty = true;
   // compiled per-node op ranges
   std::vector<ExecDesc> per_node;
+  std::vector<OpDev> h_ops;         // host copy of the compiled op lists (copy-engine executor)
   int dev = 0;
   NodeDev* d_nodes = nullptr;
   BlockDev* d_blocks = nullptr;
@@ -175,6 +384,10 @@ struct lp_mc {
   int32_t* d_recv = nullptr;
   int* d_err = nullptr;
   int max_resident = 0;
+  int direction = 1;                  // 0 push (sender executes), 1 pull (receiver executes)
+  int push_mode = 1, pull_mode = 1;   // 0 LDG/STG, 1 TMA
+  int64_t chunk_bytes = 16384;
+  int window = 3;
 };
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -223,6 +436,9 @@ static int compile(lp_mc* mc) {
       held_at[(size_t)r.rcv * mc->n_blocks + r.blk] = r.step;
     }
   }
+  // executor of a transfer: its sender pushes (direction 0) unless the sender
+  // is a HOST node; with direction 1 every transfer is pulled by its receiver
+  auto pulled = [&](const Row& r) { return mc->direction == 1 || mc->nodes[r.snd].kind == LP_NODE_HOST; };
   std::vector<OpDev> ops;
   std::vector<int32_t> recv;
   mc->per_node.assign(N, ExecDesc{});
@@ -231,16 +447,16 @@ static int compile(lp_mc* mc) {
     d.node = n;
     d.push_b = (int)ops.size();
     for (const Row& r : rows)
-      if (r.snd == n && mc->nodes[n].kind == LP_NODE_GPU)
-        ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1});
+      if (r.snd == n && !pulled(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1});
     d.push_e = (int)ops.size();
     d.pull_b = (int)ops.size();
     for (const Row& r : rows)
-      if (r.rcv == n && mc->nodes[r.snd].kind == LP_NODE_HOST) ops.push_back(OpDev{r.blk, r.snd, r.rcv, 0});
+      if (r.rcv == n && pulled(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1});
     d.pull_e = (int)ops.size();
+    // tiles other nodes push into n: waited for before n's kernel completes
     d.recv_b = (int)recv.size();
     for (const Row& r : rows)
-      if (r.rcv == n) recv.push_back(r.blk);
+      if (r.rcv == n && !pulled(r)) recv.push_back(r.blk);
     d.recv_e = (int)recv.size();
   }
   LP_CUDA(cudaSetDevice(mc->dev));
@@ -248,6 +464,7 @@ static int compile(lp_mc* mc) {
   if (mc->d_recv) cudaFree(mc->d_recv);
   mc->d_ops = nullptr;
   mc->d_recv = nullptr;
+  mc->h_ops = ops;
   LP_CUDA(cudaMalloc(&mc->d_ops, sizeof(OpDev) * std::max<size_t>(1, ops.size())));
   LP_CUDA(cudaMalloc(&mc->d_recv, sizeof(int32_t) * std::max<size_t>(1, recv.size())));
   if (!ops.empty()) LP_CUDA(cudaMemcpy(mc->d_ops, ops.data(), sizeof(OpDev) * ops.size(), cudaMemcpyHostToDevice));
@@ -294,11 +511,6 @@ int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_of
   }
   cudaMemcpy(mc->d_blocks, mc->blocks.data(), sizeof(BlockDev) * n_blocks, cudaMemcpyHostToDevice);
   cudaMemset(mc->d_err, 0, sizeof(int));
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc_kernel, LP_MC_THREADS, 0);
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, mc->dev);
-  mc->max_resident = occ * sms;
   *out = mc;
   return 0;
 }
@@ -353,15 +565,38 @@ int lp_mc_reset_signals(lp_mc* mc, int node, void* stream) {
   return 0;
 }
 
+int lp_mc_configure(lp_mc* mc, int direction, int push_mode, int pull_mode, int64_t chunk_bytes,
+                    int window) {
+  LP_CHECK(mc, "lp_mc_configure: null handle");
+  LP_CHECK(direction == 0 || direction == 1, "lp_mc_configure: direction is 0 (push) or 1 (pull)");
+  LP_CHECK((push_mode == 0 || push_mode == 1) && (pull_mode == 0 || pull_mode == 1),
+           "lp_mc_configure: modes are 0 (ldg) or 1 (tma)");
+  LP_CHECK(chunk_bytes >= 1024 && chunk_bytes % 16 == 0 && chunk_bytes * kStages <= 216 * 1024,
+           "lp_mc_configure: chunk_bytes must be a multiple of 16 in [1024, %d]", 216 * 1024 / kStages);
+  LP_CHECK(chunk_bytes <= mc->tile_bytes, "lp_mc_configure: chunk larger than a tile");
+  if (direction != mc->direction) mc->dirty = true;
+  if (window >= 1) mc->window = window < kMaxWindow ? window : kMaxWindow;
+  mc->direction = direction;
+  mc->push_mode = push_mode;
+  mc->pull_mode = pull_mode;
+  mc->chunk_bytes = chunk_bytes;
+  return 0;
+}
+
 int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch, int push_ctas,
               int pull_ctas, void* stream) {
   LP_CHECK(mc && n_exec >= 1 && n_exec <= LP_MAX_EXEC, "lp_mc_run: n_exec must be in [1, %d]", LP_MAX_EXEC);
   LP_CHECK(epoch >= 1, "lp_mc_run: epoch must be >= 1");
-  LP_CHECK(push_ctas >= 1 && pull_ctas >= 0, "lp_mc_run: need push_ctas >= 1, pull_ctas >= 0");
+  LP_CHECK(push_ctas >= 0 && pull_ctas >= 0 && push_ctas + pull_ctas >= 1, "lp_mc_run: bad CTA counts");
   const int per = push_ctas + pull_ctas;
-  LP_CHECK(per * n_exec <= mc->max_resident,
-           "lp_mc_run: %d CTAs exceed the %d co-resident CTAs the dataflow needs", per * n_exec,
-           mc->max_resident);
+  const bool any_tma = (push_ctas > 0 && mc->push_mode == 1) || (pull_ctas > 0 && mc->pull_mode == 1);
+  const int smem = any_tma ? (int)(kStages * mc->chunk_bytes) : 0;
+  LP_CUDA(cudaFuncSetAttribute(mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem > 0 ? smem : 0));
+  int occ = 0, sms = 0;
+  LP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mc_kernel, LP_MC_THREADS, smem));
+  LP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, mc->dev));
+  LP_CHECK(per * n_exec <= occ * sms,
+           "lp_mc_run: %d CTAs exceed the %d co-resident CTAs the dataflow needs", per * n_exec, occ * sms);
   if (mc->dirty && compile(mc) != 0) return -2;
   McParams p{};
   p.nodes = mc->d_nodes;
@@ -372,17 +607,95 @@ int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch, 
   p.tile_bytes = mc->tile_bytes;
   p.timeout_ns = 20ull * 1000 * 1000 * 1000;
   p.epoch = epoch;
+  p.chunk_bytes = (uint32_t)mc->chunk_bytes;
   p.push_ctas = push_ctas;
   p.pull_ctas = pull_ctas;
+  p.push_mode = mc->push_mode;
+  p.pull_mode = mc->pull_mode;
   p.n_exec = n_exec;
+  p.window = mc->window;
   for (int i = 0; i < n_exec; ++i) {
     int n = exec_nodes[i];
     LP_CHECK(n >= 0 && n < mc->n_nodes, "lp_mc_run: exec node %d out of range", n);
     LP_CHECK(mc->nodes[n].kind == LP_NODE_GPU, "lp_mc_run: exec node %d is not a GPU node", n);
     p.exec[i] = mc->per_node[n];
   }
-  mc_kernel<<<per * n_exec, LP_MC_THREADS, 0, (cudaStream_t)stream>>>(p);
+  mc_kernel<<<per * n_exec, LP_MC_THREADS, smem, (cudaStream_t)stream>>>(p);
   LP_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Copy-engine executor.  Same transfer set, same tile flags, but every tile is
+// moved by a DMA copy engine: the receiver's stream waits (cuStreamWaitValue32)
+// until the sender's flag for the tile holds the epoch, issues a
+// cudaMemcpyAsync of the tile (peer NVLink read, or PCIe from pinned host
+// memory) and then publishes its own flag with a fenced cuStreamWriteValue32.
+// Copy engines keep ~778 GB/s per direction while a GPU both sends and
+// receives, where SM-issued peer traffic drops to ~673 GB/s
+// (tools/p2p_micro.cu, profiles/), and they leave every SM free for
+// execute-while-load serving.  Ops are dealt round-robin over `n_streams`
+// streams so one slow upstream does not idle the node's ingress.
+// driver entry points resolved through the runtime (no link-time libcuda
+// dependency, so the library loads on CPU-only hosts for the ABI checks)
+typedef CUresult (*PFN_waitv32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_writev32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_waitv32 g_wait32 = nullptr;
+static PFN_writev32 g_write32 = nullptr;
+
+static int resolve_stream_memops() {
+  if (g_wait32 && g_write32) return 0;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  LP_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q));
+  LP_CHECK(q == cudaDriverEntryPointSuccess && fn, "cuStreamWaitValue32 unavailable");
+  g_wait32 = (PFN_waitv32)fn;
+  LP_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q));
+  LP_CHECK(q == cudaDriverEntryPointSuccess && fn, "cuStreamWriteValue32 unavailable");
+  g_write32 = (PFN_writev32)fn;
+  return 0;
+}
+#define cuStreamWaitValue32 g_wait32
+#define cuStreamWriteValue32 g_write32
+
+int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
+                 void* const* block_events) {
+  if (resolve_stream_memops() != 0) return -1;
+  LP_CHECK(mc && node >= 0 && node < mc->n_nodes, "lp_mc_run_ce: bad node");
+  LP_CHECK(epoch >= 1 && n_streams >= 1 && streams, "lp_mc_run_ce: bad arguments");
+  LP_CHECK(mc->direction == 1, "lp_mc_run_ce: copy-engine execution is receiver-driven (direction 1)");
+  LP_CHECK(mc->nodes[node].kind == LP_NODE_GPU, "lp_mc_run_ce: node %d is not a GPU node", node);
+  if (mc->dirty && compile(mc) != 0) return -2;
+  const ExecDesc ex = mc->per_node[node];
+  const NodeDev me = mc->nodes[node];
+  for (int oi = ex.pull_b; oi < ex.pull_e; ++oi) {
+    const OpDev op = mc->h_ops[oi];
+    const BlockDev bl = mc->blocks[op.block];
+    const NodeDev src = mc->nodes[op.src];
+    CUstream s = (CUstream)streams[(oi - ex.pull_b) % n_streams];
+    for (int t = 0; t < bl.ntiles; ++t) {
+      const int64_t lo = (int64_t)t * mc->tile_bytes;
+      const int64_t n = std::min<int64_t>(mc->tile_bytes, bl.len - lo);
+      if (op.wait) {
+        CUresult r = cuStreamWaitValue32(s, (CUdeviceptr)(src.flags + bl.tile_base + t), epoch,
+                                         CU_STREAM_WAIT_VALUE_GEQ);
+        LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWaitValue32 failed (%d)", (int)r);
+      }
+      LP_CUDA(cudaMemcpyAsync(me.image + bl.off + lo, src.image + bl.off + lo, (size_t)n, cudaMemcpyDefault,
+                              (cudaStream_t)s));
+      CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(me.flags + bl.tile_base + t), epoch,
+                                        CU_STREAM_WRITE_VALUE_DEFAULT);
+      LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
+    }
+    CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(me.counts + op.block), epoch * (uint32_t)bl.ntiles,
+                                      CU_STREAM_WRITE_VALUE_DEFAULT);
+    LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
+    if (me.ready) {
+      r = cuStreamWriteValue32(s, (CUdeviceptr)(me.ready + op.block), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+      LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: ready write failed (%d)", (int)r);
+    }
+    if (block_events && block_events[op.block]) LP_CUDA(cudaEventRecord((cudaEvent_t)block_events[op.block], (cudaStream_t)s));
+  }
   return 0;
 }
 

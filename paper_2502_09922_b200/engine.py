@@ -94,12 +94,26 @@ class MulticastEngine:
         arr = N.i32_array(flat) if flat else (C.c_int32 * 1)()
         N.call("lp_mc_set_schedule", self._h, arr, len(rows), N.i32_array(list(sources)), len(sources))
 
+    def configure(self, direction: int = 1, push_mode: int = 1, pull_mode: int = 1, chunk_bytes: int = 16384,
+                  window: int = 3):
+        """direction 0 = senders push, 1 = receivers pull; copy engine per role:
+        0 = LDG/STG vectors, 1 = TMA bulk pipeline; window = ops an LDG CTA may interleave."""
+        N.call("lp_mc_configure", self._h, direction, push_mode, pull_mode, chunk_bytes, window)
+
     def reset_signals(self, node: int, stream: int = 0):
         N.call("lp_mc_reset_signals", self._h, node, C.c_void_p(stream or None))
 
     def run(self, exec_nodes, epoch: int, push_ctas: int, pull_ctas: int, stream: int = 0):
         N.call("lp_mc_run", self._h, N.i32_array(list(exec_nodes)), len(exec_nodes), epoch,
                push_ctas, pull_ctas, C.c_void_p(stream or None))
+
+    def run_ce(self, node: int, epoch: int, streams: list, block_events: list | None = None):
+        """Enqueue ``node``'s receives on copy engines (see lp_mc_run_ce)."""
+        arr = (C.c_void_p * len(streams))(*[int(x) for x in streams])
+        evs = None
+        if block_events is not None:
+            evs = (C.c_void_p * self.n_blocks)(*[int(e) if e else None for e in block_events])
+        N.call("lp_mc_run_ce", self._h, node, epoch, len(streams), arr, evs)
 
     def status(self, stream: int = 0) -> None:
         code = C.c_int()
@@ -320,10 +334,45 @@ class Cluster:
             epoch = self.epoch
         else:
             self.epoch = epoch
-        if push_ctas < 1:
-            raise InvalidArgumentError("push_ctas must be >= 1")
+        if push_ctas < 0 or pull_ctas < 0 or push_ctas + pull_ctas < 1:
+            raise InvalidArgumentError("need at least one CTA")
         self.engine.run(self.exec_nodes, epoch, push_ctas, pull_ctas, stream)
         return epoch
+
+    def ce_streams(self, node: int, count: int = 2) -> list:
+        """Per-node torch streams the copy-engine executor enqueues on."""
+        import torch
+        if not hasattr(self, "_ce"):
+            self._ce = {}
+        if node not in self._ce or len(self._ce[node]) != count:
+            dev = torch.cuda.current_device()
+            self._ce[node] = [torch.cuda.Stream(device=dev) for _ in range(count)]
+        return self._ce[node]
+
+    def launch_ce(self, streams_per_node: int = 2, epoch: int | None = None, after=None) -> int:
+        """One epoch on copy engines for every exec node; ``after`` = a torch
+        event the CE streams wait for first.  Returns the epoch."""
+        if epoch is None:
+            self.epoch += 1
+            epoch = self.epoch
+        else:
+            self.epoch = epoch
+        for node in self.exec_nodes:
+            streams = self.ce_streams(node, streams_per_node)
+            if after is not None:
+                for st in streams:
+                    st.wait_event(after)
+            self.engine.run_ce(node, epoch, [st.cuda_stream for st in streams])
+        return epoch
+
+    def join_ce(self, stream) -> None:
+        """Make ``stream`` wait for every CE stream of this process."""
+        import torch
+        for node in self.exec_nodes:
+            for st in self.ce_streams(node):
+                ev = torch.cuda.Event()
+                ev.record(st)
+                stream.wait_event(ev)
 
     def wait(self, stream: int = 0):
         try:

@@ -1,0 +1,174 @@
+"""``scale_out``: the reference's λScale launch sequence on real GPUs.
+
+Mirrors ``_Engine._launch_lambda_scale`` (simengine.py:564-602): startup
+classes and sources (modelmgr.startup_plan), ``k_eff = min(|sources|, |cold|,
+k)``, sub-groups + k-way orders, ``compose_schedule``, completion-ordered
+groups, execution pipelines with activation steps — then, instead of pushing
+modelled ``transfer_step_done`` events, it executes the schedule with the
+CUDA multicast engine and reports measured times.
+
+Node numbering follows the reference CLI (cli.py:308-309): ``nodes[:k]`` are
+the sources.  On one box a node is a GPU (rank); a HOST node (pinned memory)
+is node 0 when the source tier is host memory (config C3).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+from . import engine as E
+from .cluster import ClusterSpec, b200_box, transfer_step_time
+from .image import CONFIGS, ImageLayout, LlamaConfig, build_layout, model_spec
+from .multicast import (MulticastSchedule, attach_orders, compose_schedule, k_way_orders,
+                        partition_subgroups, schedule_to_lines, select_block_count)
+from .pipeline import assign_blocks_to_stages, completion_ordered_groups, generate_pipelines
+
+
+@dataclass
+class ScaleOutPlan:
+    config: LlamaConfig
+    layout: ImageLayout
+    nodes: list
+    sources: list
+    groups: list
+    schedule: MulticastSchedule
+    ordered: list
+    pipelines: list
+    step_s_model: float
+    host_source: bool = False
+
+    @property
+    def block_count(self) -> int:
+        return self.layout.plan.block_count
+
+    @property
+    def receivers(self) -> list:
+        return [n for n in self.nodes if n not in self.sources]
+
+    def lines(self) -> list:
+        return schedule_to_lines(self.schedule)
+
+
+def plan_scale_out(config, n_nodes: int, k: int = 1, block_count="auto",
+                   cluster: ClusterSpec | None = None, host_source: bool = False) -> ScaleOutPlan:
+    """Planning half of ``_launch_lambda_scale`` (simengine.py:579-590)."""
+    cfg = CONFIGS[config] if isinstance(config, str) else config
+    cluster = cluster or b200_box(node_count=n_nodes)
+    spec = model_spec(cfg)
+    if block_count == "auto":
+        block_count = select_block_count(spec, n_nodes, cluster.step_fixed_overhead_s, cluster.nic_Bps)
+    layout = build_layout(cfg, int(block_count))
+    nodes = list(range(n_nodes))
+    k_eff = max(1, min(k, n_nodes - 1)) if n_nodes > 1 else 1
+    sources = nodes[:k_eff]
+    groups = attach_orders(partition_subgroups(nodes, sources), k_way_orders(layout.plan.block_count, k_eff))
+    sched = compose_schedule(groups, layout.plan, cluster.step_fixed_overhead_s, cluster.nic_Bps)
+    ordered = completion_ordered_groups(groups, sched)
+    orders = [g.transfer_order for g in ordered]
+    pipes = generate_pipelines(ordered) if any(g.receivers for g in ordered) else []
+    eps = [assign_blocks_to_stages(pn, orders, layout.plan.block_count, sched, i) for i, pn in enumerate(pipes)]
+    step_s = transfer_step_time(sched, layout.plan, cluster)
+    return ScaleOutPlan(cfg, layout, nodes, sources, groups, sched, ordered, eps, step_s, host_source)
+
+
+@dataclass
+class ScaleOutResult:
+    epoch: int
+    kernel_ms: float                 # device time of this rank's multicast kernel
+    wall_ms: float                   # host wall time launch -> complete
+    arrivals_ms: dict = field(default_factory=dict)   # node -> [per-block arrival, ms from start]
+
+
+class ScaleOut:
+    """Owns a cluster + compiled schedule; ``run()`` performs one scale-out."""
+
+    def __init__(self, plan: ScaleOutPlan, distributed: bool = False, tile_bytes: int = E.DEFAULT_TILE,
+                 push_ctas: int = 0, pull_ctas: int = 64, seed: int = 0, device: int = 0, direction: int = 1,
+                 copy_mode: int = 1, chunk_bytes: int = 16384, executor: str = "kernel", ce_streams: int = 2):
+        self.plan = plan
+        self.distributed = distributed
+        self.push_ctas, self.pull_ctas = push_ctas, pull_ctas
+        lay = plan.layout
+        if distributed:
+            self.cluster = E.Cluster.distributed(lay.block_offsets, lay.block_lengths, lay.weights_bytes,
+                                                 host_node=plan.host_source, tile_bytes=tile_bytes)
+        else:
+            n_gpu = len(plan.nodes) - (1 if plan.host_source else 0)
+            self.cluster = E.Cluster.local(n_gpu, lay.block_offsets, lay.block_lengths, lay.weights_bytes,
+                                           device=device, host_node=plan.host_source, tile_bytes=tile_bytes)
+        if executor not in ("kernel", "ce"):
+            raise ValueError("executor is 'kernel' (in-kernel NVLink/PCIe copies) or 'ce' (copy engines)")
+        self.executor = executor
+        self.ce_streams = ce_streams
+        self.cluster.engine.configure(1 if executor == "ce" else direction, copy_mode, copy_mode, chunk_bytes, 3)
+        self.seed = seed
+        self.device = device
+        self._loaded = False
+
+    def load_sources(self):
+        """Materialise the model on every source (GPU fill / host copy)."""
+        import torch.distributed as dist
+        for s in self.plan.sources:
+            nb = self.cluster.node(s)
+            mine = (nb.kind == E.LP_NODE_HOST and self.cluster.rank == 0) or \
+                (nb.kind == E.LP_NODE_GPU and s in self.cluster.exec_nodes)
+            if mine:
+                E.load_source_image(self.cluster, s, self.plan.layout, self.seed, self.device)
+        if self.distributed:
+            dist.barrier()
+        self.cluster.set_schedule(self.plan.schedule, self.plan.sources)
+        self._loaded = True
+
+    def launch(self, stream: int = 0) -> int:
+        if not self._loaded:
+            self.load_sources()
+        return self.cluster.launch(self.push_ctas, self.pull_ctas, stream)
+
+    def run(self, stream=None) -> ScaleOutResult:
+        import torch
+        s = stream or torch.cuda.current_stream()
+        sp = E.N.stream_ptr(s)
+        t0 = time.perf_counter()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(s)
+        if self.executor == "ce":
+            if not self._loaded:
+                self.load_sources()
+            epoch = self.cluster.launch_ce(self.ce_streams, after=ev0)
+            self.cluster.join_ce(s)
+            ev1.record(s)
+            s.synchronize()
+        else:
+            epoch = self.launch(sp)
+            ev1.record(s)
+            self.cluster.wait(sp)
+        wall = (time.perf_counter() - t0) * 1e3
+        return ScaleOutResult(epoch, ev0.elapsed_time(ev1), wall)
+
+    def arrivals(self, node: int) -> list:
+        return self.cluster.engine.arrivals_ns(node)
+
+    def checksums(self, node: int) -> list:
+        nb = self.cluster.node(node)
+        return E.block_checksums(nb.image, self.plan.layout.block_offsets, self.plan.layout.block_lengths)
+
+    def close(self):
+        self.cluster.close()
+
+
+def scale_out(model, sources, targets, k: int = 1, block_count="auto", host_source: bool = False,
+              distributed: bool = False, **kw):
+    """Drop-in entry: plan + execute one λPipe scale-out.
+
+    ``sources``/``targets`` are node ids; only the reference's canonical
+    ``nodes = sources + targets`` ordering is supported (cli.py:308-309).
+    Returns ``(ScaleOut, ScaleOutResult)``.
+    """
+    nodes = list(sources) + list(targets)
+    if nodes != list(range(len(nodes))):
+        raise ValueError("scale_out expects sources first, nodes numbered 0..N-1")
+    plan = plan_scale_out(model, len(nodes), k=max(k, 1), block_count=block_count, host_source=host_source)
+    so = ScaleOut(plan, distributed=distributed, **kw)
+    so.load_sources()
+    return so, so.run()

@@ -32,7 +32,8 @@ def oracle_sums():
     return get
 
 
-def run_case(n, k, b, host, tile, push, pull, oracle_sums, epochs=2):
+def run_case(n, k, b, host, tile, push, pull, oracle_sums, epochs=2, push_mode=1, pull_mode=0, chunk=16384,
+             direction=0, executor="kernel"):
     lay = I.build_layout(CFG, b)
     n_gpu = n - (1 if host else 0)
     cl = E.Cluster.local(n_gpu, lay.block_offsets, lay.block_lengths, lay.weights_bytes,
@@ -46,12 +47,19 @@ def run_case(n, k, b, host, tile, push, pull, oracle_sums, epochs=2):
         for s in sources:
             E.load_source_image(cl, s, lay, SEED)
         cl.set_schedule(sched, sources)
+        cl.engine.configure(direction, push_mode, pull_mode, chunk)
         want = oracle_sums(b)
         for ep in range(epochs):
             for i in nodes[k:]:
                 E.N.call("lp_memset", E.C.c_void_p(cl.node(i).image), 0, lay.weights_bytes, None)
-            cl.launch(push_ctas=push, pull_ctas=pull)
-            cl.wait()
+            if executor == "ce":
+                import torch
+                cl.launch_ce(2)
+                cl.join_ce(torch.cuda.current_stream())
+                torch.cuda.synchronize()
+            else:
+                cl.launch(push_ctas=push, pull_ctas=pull)
+                cl.wait()
             for i in nodes:
                 if cl.node(i).kind != E.LP_NODE_GPU:
                     continue
@@ -77,8 +85,23 @@ def run_case(n, k, b, host, tile, push, pull, oracle_sums, epochs=2):
     (9, 2, 8, True, 512 * 1024, 4, 4),   # host + GPU source mix (k=2)
     (3, 1, 3, False, 4096, 2, 0),
 ])
-def test_multicast_delivers_source_bytes(n, k, b, host, tile, push, pull, oracle_sums):
-    run_case(n, k, b, host, tile, push, pull, oracle_sums)
+@pytest.mark.parametrize("direction,push_mode,pull_mode", [(0, 0, 0), (0, 1, 0), (0, 1, 1), (1, 0, 0), (1, 0, 1)])
+def test_multicast_delivers_source_bytes(n, k, b, host, tile, push, pull, direction, push_mode, pull_mode,
+                                         oracle_sums):
+    if direction == 0 and pull_mode == 1 and not host:
+        pytest.skip("pull mode only matters with a host source")
+    chunk = min(16384, tile)
+    if direction == 1:
+        pull = max(pull, push)
+    run_case(n, k, b, host, tile, push, pull, oracle_sums, push_mode=push_mode, pull_mode=pull_mode,
+             chunk=chunk, direction=direction)
+
+
+@pytest.mark.parametrize("n,k,b,host,tile", [(4, 1, 4, False, 1 << 20), (8, 2, 8, False, 1 << 20),
+                                             (9, 1, 8, True, 2 << 20), (9, 2, 8, True, 1 << 20),
+                                             (5, 1, 1, False, 4096)])
+def test_copy_engine_executor_delivers_source_bytes(n, k, b, host, tile, oracle_sums):
+    run_case(n, k, b, host, tile, 0, 1, oracle_sums, direction=1, executor="ce")
 
 
 def test_engine_rejects_bad_schedules():
