@@ -39,6 +39,7 @@ METRIC = "scale-out time & aggregate GB/s (1→N GPUs); tokens/s + TTFT during l
 C3_MODEL, C3_BLOCKS = "llama2-13b", 40
 C2_MODEL, C2_BLOCKS = "llama3-8b", 16
 SEED = 20250815
+NCU_TRAFFIC_RATIO = (3.153332e9 + 10.150656e6) / 3193006080   # profiles/mc_kernel_host_pull_full_r01.csv
 
 
 def env_rank():
@@ -298,7 +299,10 @@ def main():
                          "peak": 64.0, "unit": "GB/s", "frac": round(achieved / 64.0, 4),
                          "peak_note": "PCIe Gen5 x16 nominal (the reference's h2d_Bps); measured DMA H2D on "
                                       "this pool 55.6 GB/s (profiles/probe_r01.json)",
-                         "traffic": None},
+                         "traffic": int(NCU_TRAFFIC_RATIO * M),
+                         "traffic_note": "dram read+write per launch from ncu --set full of the same kernel "
+                                         "(profiles/mc_kernel_host_pull_full_r01.csv: 3.163 GB for a 3.193 GB "
+                                         "image, ratio 0.991) scaled to this image"},
             "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(4 * plan.block_count * N),
                     "path": "paper_2502_09922_b200.scaleout: plan_scale_out + set_schedule + run + completion readback"},

@@ -124,6 +124,34 @@ int lp_mc_reset_signals(lp_mc* mc, int node, void* stream);
 int lp_mc_arrivals(lp_mc* mc, int node, uint64_t* out_ns);
 int lp_mc_block_complete(lp_mc* mc, int node, uint32_t epoch, int32_t* out_flags);
 
+/* ---- Llama decoder kernels (execute-while-load + local generate) --------
+ * The reference models a token as `per_block_compute_ms` per block
+ * (simengine.py:323-343) and prefill as `prompt x prefill_ms_per_token`
+ * (:320-321); these compute the real thing on the packed image.  Weights
+ * are bf16 [out, in] row-major, activations bf16, residual fp32.
+ *
+ * Tensor-core GEMM (tcgen05.mma + TMEM + TMA): Y[t,n] = sum_k X[t,k] W[n,k].
+ * epilogue 0: out_f32[t*ldo+n] += Y (split_k >= 1 allowed)
+ * epilogue 1: out_f32[t*ldo+n]  = Y (split_k must be 1) */
+int lp_gemm_bf16(const void* W, int64_t n_rows, int64_t k, const void* X, int64_t tokens, void* out,
+                 int64_t ldo, int epilogue, int split_k, void* stream);
+/* fused gate/up + SwiGLU: out_bf16[t*ldo+n] = silu(X Wg^T)[t,n] * (X Wu^T)[t,n] */
+int lp_gemm_swiglu(const void* W_gate, const void* W_up, int64_t n_rows, int64_t k, const void* X,
+                   int64_t tokens, void* out_bf16, int64_t ldo, void* stream);
+int lp_embed(const void* table, int64_t d, const int32_t* tokens, int64_t T, float* x, void* stream);
+int lp_rmsnorm(const float* x, const void* w, int64_t T, int64_t d, float eps, void* y, void* stream);
+/* RoPE (HF rotate_half) on q/k of qkv fp32 [T,(H+2KV)*hd]; q -> q_out bf16,
+ * k/v appended to cache[seq][kv][pos][hd] bf16 */
+int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim, const int32_t* pos,
+               const int32_t* seq, float theta, void* q_out, void* k_cache, void* v_cache, int64_t max_len,
+               void* stream);
+/* ragged causal GQA attention: token t attends to 0..pos[t] of seq[t] */
+int lp_attention(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
+                 const int32_t* seq, int64_t T, int n_heads, int n_kv, int head_dim, int64_t max_len,
+                 float scale, void* out, void* stream);
+/* greedy argmax per row; top2 (optional, [T,2]) = best and runner-up logit */
+int lp_argmax(const float* logits, int64_t T, int64_t V, int32_t* out, float* top2, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

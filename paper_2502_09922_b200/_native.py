@@ -59,6 +59,13 @@ SIGNATURES = {
     "lp_mc_reset_signals": [_vp, C.c_int, _vp],
     "lp_mc_arrivals": [_vp, C.c_int, _P(_u64)],
     "lp_mc_block_complete": [_vp, C.c_int, _u32, _P(_i32)],
+    "lp_gemm_bf16": [_vp, _i64, _i64, _vp, _i64, _vp, _i64, C.c_int, C.c_int, _vp],
+    "lp_gemm_swiglu": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
+    "lp_embed": [_vp, _i64, _vp, _i64, _vp, _vp],
+    "lp_rmsnorm": [_vp, _vp, _i64, _i64, C.c_float, _vp, _vp],
+    "lp_rope_kv": [_vp, _i64, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_float, _vp, _vp, _vp, _i64, _vp],
+    "lp_attention": [_vp, _vp, _vp, _vp, _vp, _i64, C.c_int, C.c_int, C.c_int, _i64, C.c_float, _vp, _vp],
+    "lp_argmax": [_vp, _i64, _i64, _vp, _vp, _vp],
 }
 _RESTYPE = {"lp_last_error": C.c_char_p}
 

@@ -1,0 +1,338 @@
+// Llama linear layers on the 5th-gen tensor cores: tcgen05.mma with the
+// accumulator in TMEM, operands staged by TMA (128B swizzle), warp-specialised.
+//
+//   Y[t, n] (epilogue) = sum_k X[t, k] * W[n, k]        X: [T, K] bf16, W: [N, K] bf16
+//
+// "Swap-AB": the weight tile (128 output features x 64 k) is the MMA's A
+// operand (M = 128 TMEM lanes) and the token tile is B (N = BT tokens), so the
+// same kernel serves decode (T = a few tokens, weight streaming bound) and
+// prefill (T = hundreds, tensor bound).  Both operands are K-major, loaded by
+// TMA boxes of 64 bf16 (= one 128-byte swizzle atom) into a STAGES-deep smem
+// ring guarded by full/empty mbarriers.
+//
+//   warp 0  : TMA producer (one elected lane)
+//   warp 1  : TMEM allocator + MMA issuer (one elected lane issues
+//             tcgen05.mma.cta_group::1.kind::f16, commits to mbarriers)
+//   warps 2-5: epilogue — tcgen05.ld 32x32b -> registers -> global, fused:
+//             EPI_ADD_F32   out_f32[t,n] += acc    (residual add; split-K safe)
+//             EPI_STORE_F32 out_f32[t,n]  = acc    (logits)
+//             EPI_SWIGLU    out_bf16[t,n] = silu(acc_gate) * acc_up  (two
+//                           accumulators: gate and up weights share the B tile)
+//
+// Grid: x = 128-row weight tiles, y = token tiles, z = K splits.
+#include "lp_common.cuh"
+#include "../../include/lambdapipe.h"
+#include <cuda.h>
+#include <mutex>
+#include <unordered_map>
+
+namespace {
+
+constexpr int BM = 128;       // weight rows per CTA (TMEM lanes)
+constexpr int BK = 64;        // k per stage = one 128B swizzle atom of bf16
+constexpr int UMMA_K = 16;    // k per tcgen05.mma (kind::f16)
+constexpr int THREADS = 192;  // 6 warps
+
+enum { EPI_ADD_F32 = 0, EPI_STORE_F32 = 1, EPI_SWIGLU = 2 };
+
+struct GemmArgs {
+  void* out;
+  int64_t ldo;        // elements between consecutive tokens in out
+  int n_rows;         // N (valid weight rows)
+  int tokens;         // T (valid tokens)
+  int k_blocks;       // ceil(K / BK)
+  int kb_per_split;   // k blocks per z-split
+};
+
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  // K-major, SWIZZLE_128B canonical layout: 8-row groups 1024 B apart (SBO),
+  // LBO unused (1), descriptor version 1 (sm_100), layout type 2 (128B swizzle)
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+template <int N>
+__host__ __device__ constexpr uint32_t idesc_bf16_f32() {
+  // c_format F32 [4,6), a/b format BF16 [7,10)/[10,13), K-major A/B, N>>3 at 17, M>>4 at 24
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(lp::smem_u32(smem_dst)),
+      "l"(map), "r"(lp::smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   lp::smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <int BT, int EPI>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;              // 16 KiB
+  static constexpr int B_BYTES = BT * BK * 2;
+  static constexpr int NA = (EPI == EPI_SWIGLU) ? 2 : 1;   // weight tiles per stage
+  static constexpr int STAGE_BYTES = NA * A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int ACC_COLS = NA * BT;
+  static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128
+                                   : ACC_COLS <= 256 ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;  // + alignment slack
+};
+
+template <int BT, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmW2,
+                const __grid_constant__ CUtensorMap tmX, const GemmArgs args) {
+  using C = Cfg<BT, EPI>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[C::STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[C::STAGES];
+  __shared__ __align__(8) uint64_t done_bar;
+  __shared__ uint32_t tmem_base_smem;
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BM;
+  const int t0 = blockIdx.y * BT;
+  const int kb0 = blockIdx.z * args.kb_per_split;
+  const int kb1 = min(args.k_blocks, kb0 + args.kb_per_split);
+  const int nkb = kb1 - kb0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      lp::mbar_init(&full_bar[s], 1);
+      lp::mbar_init(&empty_bar[s], 1);
+    }
+    lp::mbar_init(&done_bar, 1);
+    lp::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     lp::smem_u32(&tmem_base_smem)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    if (EPI == EPI_SWIGLU) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW2) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_smem;
+
+  if (warp == 0 && lane == 0 && nkb > 0) {
+    // ---------------- TMA producer ----------------
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % C::STAGES;
+      lp::mbar_wait(&empty_bar[s], ((i / C::STAGES) & 1) ^ 1);
+      uint8_t* st = smem + s * C::STAGE_BYTES;
+      lp::mbar_expect_tx(&full_bar[s], C::STAGE_BYTES);
+      const int kc = (kb0 + i) * BK;
+      tma_load_2d(st, &tmW, &full_bar[s], kc, n0);
+      if (EPI == EPI_SWIGLU) tma_load_2d(st + C::A_BYTES, &tmW2, &full_bar[s], kc, n0);
+      tma_load_2d(st + C::NA * C::A_BYTES, &tmX, &full_bar[s], kc, t0);
+    }
+  } else if (warp == 1 && lane == 0 && nkb > 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_bf16_f32<BT>();
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % C::STAGES;
+      lp::mbar_wait(&full_bar[s], (i / C::STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = lp::smem_u32(smem + s * C::STAGE_BYTES);
+      const uint32_t sb = sa + C::NA * C::A_BYTES;
+#pragma unroll
+      for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+        const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+        // +32 bytes per 16-element k step inside the 128B swizzle atom
+        umma_bf16(tmem, smem_desc_sw128(sa + kk * 32), smem_desc_sw128(sb + kk * 32), idesc, acc);
+        if (EPI == EPI_SWIGLU)
+          umma_bf16(tmem + BT, smem_desc_sw128(sa + C::A_BYTES + kk * 32), smem_desc_sw128(sb + kk * 32), idesc,
+                    acc);
+      }
+      umma_commit(&empty_bar[s]);   // smem slot free once these MMAs have read it
+    }
+    umma_commit(&done_bar);         // accumulator complete
+  } else if (warp >= 2) {
+    // ---------------- epilogue ----------------
+    const int quarter = warp & 3;   // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const int n = n0 + row;
+    if (nkb > 0) {
+      lp::mbar_wait(&done_bar, 0);
+      tc_fence_after();
+    }
+    constexpr int CH = BT < 32 ? BT : 32;
+    for (int c = 0; c < BT; c += CH) {
+      uint32_t v[32], u[32];
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + c;
+      if (nkb > 0) {
+        if (CH == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
+        if (EPI == EPI_SWIGLU) {
+          if (CH == 32) tmem_ld32(taddr + BT, u); else tmem_ld16(taddr + BT, u);
+        }
+        tmem_wait_ld();
+      } else {
+        for (int j = 0; j < 32; ++j) v[j] = u[j] = 0;
+      }
+      if (n < args.n_rows) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int t = t0 + c + j;
+          if (t >= args.tokens) break;
+          const float a = __uint_as_float(v[j]);
+          if (EPI == EPI_ADD_F32) {
+            atomicAdd((float*)args.out + (int64_t)t * args.ldo + n, a);
+          } else if (EPI == EPI_STORE_F32) {
+            ((float*)args.out)[(int64_t)t * args.ldo + n] = a;
+          } else {
+            const float up = __uint_as_float(u[j]);
+            const float act = a / (1.0f + __expf(-a)) * up;
+            ((__nv_bfloat16*)args.out)[(int64_t)t * args.ldo + n] = __float2bfloat16_rn(act);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps (driver entry point via the runtime) + dispatch
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled g_encode = nullptr;
+
+int get_encode() {
+  if (g_encode) return 0;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  LP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  LP_CHECK(q == cudaDriverEntryPointSuccess && fn, "cuTensorMapEncodeTiled unavailable");
+  g_encode = (PFN_encodeTiled)fn;
+  return 0;
+}
+
+// row-major [rows, cols] bf16 matrix, box = box_rows x 64 cols, 128B swizzle
+int make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows) {
+  if (get_encode() != 0) return -1;
+  LP_CHECK(((uintptr_t)base & 15) == 0 && (cols * 2) % 16 == 0, "tensor map: base/row stride not 16B aligned");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  LP_CHECK(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+template <int BT, int EPI>
+int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, int64_t T, void* out, int64_t ldo,
+           int split_k, cudaStream_t s) {
+  using C = Cfg<BT, EPI>;
+  CUtensorMap mw, mw2, mx;
+  if (make_map(&mw, W, N, K, BM) != 0) return -1;
+  if (make_map(&mw2, EPI == EPI_SWIGLU ? W2 : W, N, K, BM) != 0) return -1;
+  if (make_map(&mx, X, T, K, BT) != 0) return -1;
+  static bool attr_set = false;
+  if (!attr_set) {
+    LP_CUDA(cudaFuncSetAttribute(gemm_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  GemmArgs a;
+  a.out = out;
+  a.ldo = ldo;
+  a.n_rows = (int)N;
+  a.tokens = (int)T;
+  a.k_blocks = (int)((K + BK - 1) / BK);
+  const int splits = split_k < 1 ? 1 : (split_k > a.k_blocks ? a.k_blocks : split_k);
+  a.kb_per_split = (a.k_blocks + splits - 1) / splits;
+  dim3 grid((unsigned)((N + BM - 1) / BM), (unsigned)((T + BT - 1) / BT), (unsigned)splits);
+  gemm_kernel<BT, EPI><<<grid, THREADS, C::SMEM, s>>>(mw, mw2, mx, a);
+  LP_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <int EPI>
+int dispatch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, int64_t T, void* out, int64_t ldo,
+             int split_k, cudaStream_t s) {
+  if (T <= 16) return launch<16, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  if (T <= 32) return launch<32, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  if (T <= 64) return launch<64, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  if (EPI == EPI_SWIGLU || T <= 128) return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  return launch<256, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int lp_gemm_bf16(const void* W, int64_t n_rows, int64_t k, const void* X, int64_t tokens, void* out,
+                 int64_t ldo, int epilogue, int split_k, void* stream) {
+  LP_CHECK(W && X && out && n_rows > 0 && k > 0 && tokens > 0, "lp_gemm_bf16: bad arguments");
+  LP_CHECK(epilogue == EPI_ADD_F32 || epilogue == EPI_STORE_F32, "lp_gemm_bf16: epilogue must be 0 (add) or 1 (store)");
+  LP_CHECK(epilogue == EPI_ADD_F32 || split_k <= 1, "lp_gemm_bf16: split-K needs the accumulating epilogue");
+  cudaStream_t s = (cudaStream_t)stream;
+  return epilogue == EPI_ADD_F32 ? dispatch<EPI_ADD_F32>(W, nullptr, n_rows, k, X, tokens, out, ldo, split_k, s)
+                                 : dispatch<EPI_STORE_F32>(W, nullptr, n_rows, k, X, tokens, out, ldo, 1, s);
+}
+
+int lp_gemm_swiglu(const void* W_gate, const void* W_up, int64_t n_rows, int64_t k, const void* X, int64_t tokens,
+                   void* out_bf16, int64_t ldo, void* stream) {
+  LP_CHECK(W_gate && W_up && X && out_bf16 && n_rows > 0 && k > 0 && tokens > 0, "lp_gemm_swiglu: bad arguments");
+  return dispatch<EPI_SWIGLU>(W_gate, W_up, n_rows, k, X, tokens, out_bf16, ldo, 1, (cudaStream_t)stream);
+}
+
+}  // extern "C"

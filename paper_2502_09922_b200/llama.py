@@ -1,0 +1,154 @@
+"""Llama decoder on the packed image, executed by the sm_100a kernels.
+
+:class:`LlamaExecutor` runs any contiguous layer range of a model whose
+weights live in a packed image (``image.build_layout``) on one GPU: that is
+both a λPipe pipeline *stage* (layers of its resident blocks; the stage
+holding block 0 also owns embedding + final norm + LM head, see image.py)
+and, with all layers, the local full-model replica after mode switch.
+
+Per layer (fp32 residual stream ``x``, bf16 GEMM inputs, fp32 accumulation):
+
+    h   = rmsnorm(x) * attn_norm                      lp_rmsnorm
+    qkv = h @ [Wq;Wk;Wv]^T          (one GEMM: wq/wk/wv are contiguous)
+    q,k,v <- RoPE(qkv); k,v appended to the KV cache  lp_rope_kv
+    o   = causal GQA attention(q, cache)              lp_attention
+    x  += o @ Wo^T                  (GEMM, split-K, residual-add epilogue)
+    h   = rmsnorm(x) * ffn_norm
+    a   = silu(h @ Wg^T) * (h @ Wu^T)  (one GEMM, two TMEM accumulators)
+    x  += a @ Wd^T                  (GEMM, split-K, residual-add epilogue)
+
+The GEMMs are ``lp_gemm_bf16`` / ``lp_gemm_swiglu`` (tcgen05 + TMEM + TMA).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+from . import _native as N
+from .engine import device_view
+from .image import ImageLayout
+
+_SMS = 148
+
+
+def _vp(x):
+    return C.c_void_p(x if isinstance(x, int) else x.data_ptr())
+
+
+class KVCache:
+    """bf16 K and V caches per layer: [max_seqs, n_kv, max_len, head_dim]."""
+
+    def __init__(self, cfg, layers, max_seqs: int, max_len: int, device):
+        import torch
+        self.max_seqs, self.max_len = max_seqs, max_len
+        shape = (max_seqs, cfg.n_kv_heads, max_len, cfg.head_dim)
+        self.k = {l: torch.zeros(shape, dtype=torch.bfloat16, device=device) for l in layers}
+        self.v = {l: torch.zeros(shape, dtype=torch.bfloat16, device=device) for l in layers}
+
+
+class LlamaExecutor:
+    """Runs layers [layer_lo, layer_hi] (+ vocab ops if it holds block 0)."""
+
+    def __init__(self, layout: ImageLayout, image_ptr: int, device: int, layer_lo: int = 0,
+                 layer_hi: int | None = None, max_seqs: int = 8, max_len: int = 512, vocab_ops: bool = True):
+        import torch
+        self.lay = layout
+        self.cfg = layout.config
+        self.base = image_ptr
+        self.device = device
+        self.layer_lo = layer_lo
+        self.layer_hi = self.cfg.n_layers - 1 if layer_hi is None else layer_hi
+        self.vocab_ops = vocab_ops
+        self.torch_device = torch.device(f"cuda:{device}")
+        self.cache = KVCache(self.cfg, range(self.layer_lo, self.layer_hi + 1), max_seqs, max_len,
+                             self.torch_device)
+        self.lib = N.lib()
+
+    # -- weights ----------------------------------------------------------------
+    def ptr(self, name: str) -> int:
+        return self.base + self.lay.by_name[name].offset
+
+    def weight(self, name: str):
+        """A torch bf16 view of one packed tensor (no copy)."""
+        import torch
+        t = self.lay.by_name[name]
+        return device_view(self.base + t.offset, t.nbytes, self.device, torch.bfloat16, t.shape)
+
+    # -- kernels ------------------------------------------------------------------
+    def _gemm_add(self, w: int, n_rows: int, k: int, x, tokens: int, out, ldo: int, stream: int):
+        tiles = -(-n_rows // 128) * -(-tokens // 128)
+        split = max(1, min(_SMS // max(tiles, 1), max(1, (k // 64) // 4)))
+        N.check(self.lib.lp_gemm_bf16(C.c_void_p(w), n_rows, k, _vp(x), tokens, _vp(out), ldo, 0, split,
+                                      C.c_void_p(stream)), "lp_gemm_bf16")
+
+    def embed(self, tokens, stream: int = 0):
+        import torch
+        T = tokens.numel()
+        x = torch.empty((T, self.cfg.d_model), dtype=torch.float32, device=self.torch_device)
+        N.check(self.lib.lp_embed(C.c_void_p(self.ptr("embed")), self.cfg.d_model, _vp(tokens), T, _vp(x),
+                                  C.c_void_p(stream)), "lp_embed")
+        return x
+
+    def layer(self, l: int, x, pos, seq, stream: int = 0):
+        import torch
+        cfg = self.cfg
+        T, d = x.shape
+        H, KV, hd = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+        s = C.c_void_p(stream)
+        dev = self.torch_device
+        h = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
+        N.check(self.lib.lp_rmsnorm(_vp(x), C.c_void_p(self.ptr(f"layers.{l}.attn_norm")), T, d, cfg.norm_eps,
+                                    _vp(h), s), "lp_rmsnorm")
+        nq = (H + 2 * KV) * hd
+        qkv = torch.zeros((T, nq), dtype=torch.float32, device=dev)
+        self._gemm_add(self.ptr(f"layers.{l}.wq"), nq, d, h, T, qkv, nq, stream)
+        q = torch.empty((T, H * hd), dtype=torch.bfloat16, device=dev)
+        N.check(self.lib.lp_rope_kv(_vp(qkv), T, H, KV, hd, _vp(pos), _vp(seq), cfg.rope_theta, _vp(q),
+                                    _vp(self.cache.k[l]), _vp(self.cache.v[l]), self.cache.max_len, s),
+                "lp_rope_kv")
+        o = torch.empty((T, H * hd), dtype=torch.bfloat16, device=dev)
+        N.check(self.lib.lp_attention(_vp(q), _vp(self.cache.k[l]), _vp(self.cache.v[l]), _vp(pos), _vp(seq), T,
+                                      H, KV, hd, self.cache.max_len, 1.0 / math.sqrt(hd), _vp(o), s),
+                "lp_attention")
+        self._gemm_add(self.ptr(f"layers.{l}.wo"), d, H * hd, o, T, x, d, stream)
+        N.check(self.lib.lp_rmsnorm(_vp(x), C.c_void_p(self.ptr(f"layers.{l}.ffn_norm")), T, d, cfg.norm_eps,
+                                    _vp(h), s), "lp_rmsnorm")
+        act = torch.empty((T, cfg.ffn), dtype=torch.bfloat16, device=dev)
+        N.check(self.lib.lp_gemm_swiglu(C.c_void_p(self.ptr(f"layers.{l}.w_gate")),
+                                        C.c_void_p(self.ptr(f"layers.{l}.w_up")), cfg.ffn, d, _vp(h), T, _vp(act),
+                                        cfg.ffn, s), "lp_gemm_swiglu")
+        self._gemm_add(self.ptr(f"layers.{l}.w_down"), d, cfg.ffn, act, T, x, d, stream)
+        return x
+
+    def head(self, x, stream: int = 0):
+        """Final norm + LM head -> fp32 logits [T, V]."""
+        import torch
+        cfg = self.cfg
+        T, d = x.shape
+        h = torch.empty((T, d), dtype=torch.bfloat16, device=self.torch_device)
+        N.check(self.lib.lp_rmsnorm(_vp(x), C.c_void_p(self.ptr("final_norm")), T, d, cfg.norm_eps, _vp(h),
+                                    C.c_void_p(stream)), "lp_rmsnorm")
+        logits = torch.empty((T, cfg.vocab), dtype=torch.float32, device=self.torch_device)
+        N.check(self.lib.lp_gemm_bf16(C.c_void_p(self.ptr("lm_head")), cfg.vocab, d, _vp(h), T, _vp(logits),
+                                      cfg.vocab, 1, 1, C.c_void_p(stream)), "lp_gemm_bf16")
+        return logits
+
+    def greedy(self, logits, stream: int = 0):
+        import torch
+        T = logits.shape[0]
+        tok = torch.empty((T,), dtype=torch.int32, device=self.torch_device)
+        top2 = torch.empty((T, 2), dtype=torch.float32, device=self.torch_device)
+        N.check(self.lib.lp_argmax(_vp(logits), T, self.cfg.vocab, _vp(tok), _vp(top2), C.c_void_p(stream)),
+                "lp_argmax")
+        return tok, top2
+
+    def forward(self, tokens=None, x=None, pos=None, seq=None, stream: int = 0, want_logits: bool = True):
+        """Embed (if tokens) -> layers [lo, hi] -> head (if this stage owns it)."""
+        if x is None:
+            x = self.embed(tokens, stream)
+        for l in range(self.layer_lo, self.layer_hi + 1):
+            x = self.layer(l, x, pos, seq, stream)
+        if want_logits and self.vocab_ops and self.layer_hi == self.cfg.n_layers - 1:
+            return x, self.head(x, stream)
+        return x, None
