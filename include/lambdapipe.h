@@ -149,6 +149,12 @@ int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim,
 int lp_attention(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
                  const int32_t* seq, int64_t T, int n_heads, int n_kv, int head_dim, int64_t max_len,
                  float scale, void* out, void* stream);
+/* stage->stage activation hand-off: copy `bytes` (multiple of 16) into the
+ * next stage's buffer (peer pointer, NVLink stores); if flag != NULL, release
+ * *flag = value (sys scope) after all bytes landed (scratch: zeroed u32 on the
+ * producer, reused) */
+int lp_handoff(const void* src, void* dst, int64_t bytes, uint32_t* flag, uint32_t value, uint32_t* scratch,
+               void* stream);
 /* greedy argmax per row; top2 (optional, [T,2]) = best and runner-up logit */
 int lp_argmax(const float* logits, int64_t T, int64_t V, int32_t* out, float* top2, void* stream);
 

@@ -66,6 +66,7 @@ SIGNATURES = {
     "lp_rope_kv": [_vp, _i64, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_float, _vp, _vp, _vp, _i64, _vp],
     "lp_attention": [_vp, _vp, _vp, _vp, _vp, _i64, C.c_int, C.c_int, C.c_int, _i64, C.c_float, _vp, _vp],
     "lp_argmax": [_vp, _i64, _i64, _vp, _vp, _vp],
+    "lp_handoff": [_vp, _vp, _i64, _vp, _u32, _vp, _vp],
 }
 _RESTYPE = {"lp_last_error": C.c_char_p}
 

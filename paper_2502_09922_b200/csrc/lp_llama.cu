@@ -214,9 +214,45 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int64_t V, int32
   }
 }
 
+// Stage -> stage hand-off of the hidden state: 16-byte vector stores from
+// the producing GPU straight into the consumer's receive buffer over NVLink,
+// then (optional) a .sys release of a flag in the consumer's memory that its
+// stream waits on (cuStreamWaitValue32), so no host round trip sits between
+// pipeline stages.
+__global__ void handoff_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16, uint32_t* flag,
+                               uint32_t value, unsigned int* done_ctas) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    lp::st16(dst + i, src[i]);
+  if (flag == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    lp::fence_sys();
+    const unsigned int prev = atomicAdd(done_ctas, 1u);
+    if (prev + 1 == gridDim.x) {  // last CTA: every CTA's stores are fenced
+      *done_ctas = 0;
+      lp::fence_sys();
+      lp::st_release_sys(flag, value);
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int lp_handoff(const void* src, void* dst, int64_t bytes, uint32_t* flag, uint32_t value, uint32_t* scratch,
+               void* stream) {
+  LP_CHECK(src && dst && bytes > 0 && bytes % 16 == 0, "lp_handoff: bad arguments (bytes %% 16 == 0)");
+  LP_CHECK(!flag || scratch, "lp_handoff: a flag needs a zeroed u32 scratch counter on the producer");
+  const int64_t n16 = bytes / 16;
+  int blocks = (int)((n16 + 255) / 256);
+  if (blocks > 32) blocks = 32;
+  handoff_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((const int4*)src, (int4*)dst, n16, flag, value,
+                                                           scratch);
+  LP_CUDA(cudaGetLastError());
+  return 0;
+}
+
 
 int lp_embed(const void* table, int64_t d, const int32_t* tokens, int64_t T, float* x, void* stream) {
   LP_CHECK(table && tokens && x && T > 0 && d > 0, "lp_embed: bad arguments");

@@ -388,7 +388,14 @@ struct lp_mc {
   int push_mode = 1, pull_mode = 1;   // 0 LDG/STG, 1 TMA
   int64_t chunk_bytes = 16384;
   int window = 3;
+  cudaStream_t poll = nullptr;   // private non-blocking stream for host polls
 };
+
+static int poll_stream(lp_mc* mc) {
+  LP_CUDA(cudaSetDevice(mc->dev));
+  if (!mc->poll) LP_CUDA(cudaStreamCreateWithFlags(&mc->poll, cudaStreamNonBlocking));
+  return 0;
+}
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -523,6 +530,7 @@ int lp_mc_destroy(lp_mc* mc) {
   cudaFree(mc->d_ops);
   cudaFree(mc->d_recv);
   cudaFree(mc->d_err);
+  if (mc->poll) cudaStreamDestroy(mc->poll);
   delete mc;
   return 0;
 }
@@ -716,7 +724,10 @@ int lp_mc_status(lp_mc* mc, void* stream, int* code) {
 int lp_mc_arrivals(lp_mc* mc, int node, uint64_t* out_ns) {
   LP_CHECK(mc && node >= 0 && node < mc->n_nodes && out_ns, "lp_mc_arrivals: bad arguments");
   LP_CHECK(mc->nodes[node].arrival, "lp_mc_arrivals: node %d has no signal area", node);
-  LP_CUDA(cudaMemcpy(out_ns, mc->nodes[node].arrival, sizeof(uint64_t) * mc->n_blocks, cudaMemcpyDefault));
+  if (poll_stream(mc) != 0) return -1;
+  LP_CUDA(cudaMemcpyAsync(out_ns, mc->nodes[node].arrival, sizeof(uint64_t) * mc->n_blocks, cudaMemcpyDefault,
+                          mc->poll));
+  LP_CUDA(cudaStreamSynchronize(mc->poll));
   return 0;
 }
 
@@ -724,7 +735,10 @@ int lp_mc_block_complete(lp_mc* mc, int node, uint32_t epoch, int32_t* out_flags
   LP_CHECK(mc && node >= 0 && node < mc->n_nodes && out_flags, "lp_mc_block_complete: bad arguments");
   LP_CHECK(mc->nodes[node].counts, "lp_mc_block_complete: node %d has no signal area", node);
   std::vector<uint32_t> c(mc->n_blocks);
-  LP_CUDA(cudaMemcpy(c.data(), mc->nodes[node].counts, sizeof(uint32_t) * mc->n_blocks, cudaMemcpyDefault));
+  if (poll_stream(mc) != 0) return -1;
+  LP_CUDA(cudaMemcpyAsync(c.data(), mc->nodes[node].counts, sizeof(uint32_t) * mc->n_blocks, cudaMemcpyDefault,
+                          mc->poll));
+  LP_CUDA(cudaStreamSynchronize(mc->poll));
   for (int i = 0; i < mc->n_blocks; ++i)
     out_flags[i] = c[i] >= epoch * (uint32_t)mc->blocks[i].ntiles ? 1 : 0;
   return 0;

@@ -306,8 +306,82 @@ class Cluster:
         dist.barrier()
         return cls(eng, nodes, [rank + off], rank, world, host)
 
+    @classmethod
+    def devices(cls, node_devices: list, block_offsets, block_lengths, image_bytes: int, host_node: bool = False,
+                tile_bytes: int = DEFAULT_TILE):
+        """One process driving several GPUs: GPU node i lives on device
+        ``node_devices[i]`` (node ids shift by one if a host node 0 exists).
+        One engine per device holds the full node table; each device runs
+        one kernel over its own nodes (peer access enabled both ways)."""
+        devs = sorted(set(node_devices))
+        for a in devs:
+            for b in devs:
+                if a != b:
+                    N.call("lp_enable_peer", a, b)
+        off = 1 if host_node else 0
+        n_nodes = len(node_devices) + off
+        engines = {}
+        for d in devs:
+            N.call("lp_set_device", d)
+            engines[d] = MulticastEngine(n_nodes, block_offsets, block_lengths, tile_bytes)
+        nodes, host = [], None
+        if host_node:
+            N.call("lp_set_device", devs[0])
+            host = HostImage(image_bytes)
+            nodes.append(NodeBuffer(0, LP_NODE_HOST, -1, host.device_ptr))
+        for i, d in enumerate(node_devices):
+            img = dev_malloc(d, image_bytes)
+            sig = dev_malloc(d, engines[d].signal_bytes)
+            N.call("lp_memset", C.c_void_p(sig), 0, engines[d].signal_bytes, None)
+            nodes.append(NodeBuffer(i + off, LP_NODE_GPU, d, img, sig, [("dev", img), ("dev", sig)]))
+        for d, eng in engines.items():
+            N.call("lp_set_device", d)
+            for nb in nodes:
+                eng.set_node(nb.node, nb.kind, nb.image, nb.signals)
+        for d in devs:
+            N.call("lp_sync_device", d)
+        cl = cls(engines[devs[0]], nodes, [nb.node for nb in nodes if nb.kind == LP_NODE_GPU], host=host)
+        cl.per_device = engines
+        return cl
+
     def node(self, i: int) -> NodeBuffer:
         return self.nodes[i]
+
+    def node_device(self, i: int) -> int:
+        return self.nodes[i].device
+
+    def set_schedule_all(self, schedule, sources):
+        for d, eng in getattr(self, "per_device", {0: self.engine}).items():
+            N.call("lp_set_device", d)
+            eng.set_schedule(schedule_rows(schedule), sources)
+
+    def launch_devices(self, streams: dict, push_ctas: int = 0, pull_ctas: int = 64) -> int:
+        """Multi-device launch: one kernel per device over that device's nodes."""
+        self.epoch += 1
+        self._mc_streams = {d: (st if isinstance(st, int) else st.cuda_stream) for d, st in streams.items()}
+        streams = self._mc_streams
+        for d, eng in self.per_device.items():
+            mine = [nb.node for nb in self.nodes if nb.kind == LP_NODE_GPU and nb.device == d]
+            N.call("lp_set_device", d)
+            eng.run(mine, self.epoch, push_ctas, pull_ctas, streams[d])
+        return self.epoch
+
+    def wait_devices(self) -> None:
+        """Synchronise every per-device multicast launch; raise on a watchdog expiry."""
+        for d, eng in getattr(self, "per_device", {}).items():
+            N.call("lp_set_device", d)
+            eng.status(getattr(self, "_mc_streams", {}).get(d, 0))
+
+    def complete_nodes(self, epoch: int | None = None) -> dict:
+        """node -> per-block complete flags (reads each node's counters)."""
+        ep = self.epoch if epoch is None else epoch
+        out = {}
+        for nb in self.nodes:
+            if nb.kind != LP_NODE_GPU:
+                continue
+            eng = getattr(self, "per_device", {}).get(nb.device, self.engine)
+            out[nb.node] = eng.complete(nb.node, ep)
+        return out
 
     def close(self):
         for nb in self.nodes:
@@ -320,6 +394,8 @@ class Cluster:
         if self.host is not None:
             self.host.close(unlink=self.rank == 0 and self.host.shm_path is not None)
             self.host = None
+        for eng in getattr(self, "per_device", {}).values():
+            eng.close()
         self.engine.close()
 
     # -- execution ------------------------------------------------------------
@@ -386,6 +462,8 @@ def load_source_image(cluster: "Cluster", node: int, layout, seed: int, device: 
     nodes get a device fill copied down over PCIe)."""
     nb = cluster.node(node)
     if nb.kind == LP_NODE_GPU:
+        if nb.device >= 0:
+            N.call("lp_set_device", nb.device)
         fill_image(nb.image, layout, seed)
         return
     scratch = dev_malloc(device, layout.weights_bytes)

@@ -1,0 +1,337 @@
+"""Execute-while-load serving on real GPUs — the reference's serving units,
+activation and mode switch (simengine.py:320-389, 646-712, 736-741) with
+real tokens instead of modelled periods.
+
+While the λPipe multicast runs (``engine.Cluster.devices``, one kernel per
+GPU), receivers that hold only their pipeline stage's blocks already serve:
+
+* every :class:`~.pipeline.ExecutionPipeline` of the plan becomes a
+  pipeline unit whose stages run their resident layers (``llama.
+  LlamaExecutor``); the hidden state moves stage to stage over NVLink
+  (``lp_handoff``) and returns to the vocab stage (block 0: embedding, final
+  norm, LM head) for the next token.  A unit activates when every block its
+  stages need has *landed* (the engine's per-block tile counters) — the
+  measured counterpart of ``activation_step`` (pipeline.py:175-185);
+* capacity = stage count (pipeline.py:43-46); requests are admitted FIFO into
+  free slots of active units in unit order (``_admit``, simengine.py:356-368)
+  and batched per iteration (prefill and decode tokens in one ragged batch);
+* when every receiver holds the whole model the pipelines retire and
+  ``plan_mode_switch`` (pipeline.py:252-270) spreads their in-flight requests
+  round-robin over the pipeline's nodes, whose local units rebuild the KV
+  cache by prefilling prompt + generated tokens (the reference's recompute
+  cost), then continue decoding.
+
+Events follow the reference's ``SimEvent`` kinds/payloads (workload.py:28-32)
+with wall-clock times from the start of the scale-out, so
+``workload.aggregate`` yields TTFT percentiles and the 100 ms tokens/s
+timeline unchanged.
+"""
+
+from __future__ import annotations
+
+import time
+from collections import deque
+from dataclasses import dataclass, field
+
+from . import _native as N
+from .pipeline import plan_mode_switch
+from .workload import SimEvent, TraceRecord
+
+
+@dataclass
+class Request:
+    rec: TraceRecord
+    prompt: list
+    out: list = field(default_factory=list)
+    unit: int | None = None
+    slot: int = -1
+    kv_len: int = 0
+    needs_prefill: bool = True
+    first_token_s: float | None = None
+    done_s: float | None = None
+
+    @property
+    def rid(self) -> str:
+        return self.rec.request_id
+
+    @property
+    def done(self) -> bool:
+        return len(self.out) >= self.rec.output_tokens
+
+
+@dataclass
+class Stage:
+    node: int
+    device: int
+    block_lo: int
+    block_hi: int
+    layer_lo: int
+    layer_hi: int
+    vocab: bool
+    executor: object = None
+
+
+@dataclass
+class Unit:
+    uid: int
+    kind: str                     # pipeline | local
+    stages: list
+    slots: int
+    cold: bool
+    pipeline: object = None
+    active: bool = False
+    retired: bool = False
+    busy: dict = field(default_factory=dict)   # slot -> Request
+
+    @property
+    def nodes(self) -> tuple:
+        return tuple(st.node for st in self.stages)
+
+    @property
+    def emit_node(self) -> int:
+        return self.stages[-1].node
+
+    def free_slot(self) -> int:
+        for s in range(self.slots):
+            if s not in self.busy:
+                return s
+        return -1
+
+
+class Server:
+    """Serves a request trace while ``plan`` is being multicast."""
+
+    def __init__(self, plan, cluster, local_slots: int = 8, max_len: int = 512, switch_hold_tokens: int = 0,
+                 prefill_ms_per_token: float = 0.5):
+        import torch
+        self.plan = plan
+        self.cluster = cluster
+        self.lay = plan.layout
+        self.cfg = plan.config
+        self.local_slots = local_slots
+        self.max_len = max_len
+        self.switch_hold_tokens = switch_hold_tokens
+        self.prefill_ms_per_token = prefill_ms_per_token
+        self.events = []
+        self.units = {}
+        self._next_uid = 0
+        self.switched = False
+        self.t0 = None
+        self.torch = torch
+        self.receivers = [n for n in plan.receivers if cluster.node(n).kind == 0]
+        self.block_complete_s = {}      # node -> time it held every block
+        # pipeline units from the plan (one per ExecutionPipeline)
+        for ep in plan.pipelines:
+            stages = []
+            covered = -1
+            for st in ep.stages:
+                if st.block_lo > st.block_hi:
+                    continue                  # empty stage (reference quirk): pass-through
+                l_lo = self.lay.plan.blocks[st.block_lo].layer_lo
+                l_hi = self.lay.plan.blocks[st.block_hi].layer_hi
+                l_lo = max(l_lo, covered + 1)  # overlapped chunks (k > b) run once
+                covered = max(covered, l_hi)
+                stages.append(Stage(st.node, cluster.node_device(st.node), st.block_lo, st.block_hi, l_lo, l_hi,
+                                    st.block_lo == 0))
+            self._add_unit("pipeline", stages, max(1, len(ep.stages)), True, ep)
+
+    # -- units -------------------------------------------------------------------
+    def _add_unit(self, kind, stages, slots, cold, pipeline=None):
+        from .llama import LlamaExecutor
+        for st in stages:
+            st.executor = LlamaExecutor(self.lay, self.cluster.node(st.node).image, st.device,
+                                        st.layer_lo, st.layer_hi, max_seqs=slots, max_len=self.max_len,
+                                        vocab_ops=st.vocab)
+        u = Unit(self._next_uid, kind, stages, slots, cold, pipeline)
+        self.units[u.uid] = u
+        self._next_uid += 1
+        return u
+
+    def _local_unit(self, node):
+        dev = self.cluster.node_device(node)
+        st = Stage(node, dev, 0, self.lay.plan.block_count - 1, 0, self.cfg.n_layers - 1, True)
+        u = self._add_unit("local", [st], self.local_slots, True)
+        u.active = True
+        return u
+
+    def log(self, t, kind, **payload):
+        self.events.append(SimEvent(t, kind, payload))
+
+    # -- forward through a unit --------------------------------------------------
+    def _dev_tensor(self, vals, device):
+        return self.torch.as_tensor(vals, dtype=self.torch.int32, device=f"cuda:{device}")
+
+    def _move(self, x, src_dev, dst_dev):
+        """Hidden-state hand-off stage -> stage (NVLink stores, lp_handoff)."""
+        torch = self.torch
+        if src_dev == dst_dev:
+            return x
+        dst = torch.empty(x.shape, dtype=x.dtype, device=f"cuda:{dst_dev}")
+        with torch.cuda.device(src_dev):
+            N.check(N.lib().lp_handoff(N.C.c_void_p(x.data_ptr()), N.C.c_void_p(dst.data_ptr()),
+                                       x.numel() * x.element_size(), None, 0, None,
+                                       N.C.c_void_p(torch.cuda.current_stream(src_dev).cuda_stream)),
+                    "lp_handoff")
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(src_dev))
+        torch.cuda.current_stream(dst_dev).wait_event(ev)
+        return dst
+
+    def _forward(self, unit, tokens, pos, seq, last_idx):
+        """Run one ragged batch through the unit's stages; returns next tokens
+        (int32, on the vocab device) for rows ``last_idx``."""
+        torch = self.torch
+        vocab = next(st for st in unit.stages if st.vocab)
+        vdev = vocab.device
+        with torch.cuda.device(vdev):
+            x = vocab.executor.embed(self._dev_tensor(tokens, vdev))
+        cur = vdev
+        for st in unit.stages:
+            if st.layer_lo > st.layer_hi:
+                continue
+            x = self._move(x, cur, st.device)
+            cur = st.device
+            with torch.cuda.device(cur):
+                p, s = self._dev_tensor(pos, cur), self._dev_tensor(seq, cur)
+                ex = st.executor
+                for layer in range(st.layer_lo, st.layer_hi + 1):
+                    x = ex.layer(layer, x, p, s)
+        x = self._move(x, cur, vdev)
+        with torch.cuda.device(vdev):
+            xl = x[self._dev_tensor(last_idx, vdev).long()].contiguous()
+            logits = vocab.executor.head(xl)
+            tok, _ = vocab.executor.greedy(logits)
+        return tok
+
+    # -- scheduling --------------------------------------------------------------
+    def _admit(self, queue):
+        for u in sorted(self.units.values(), key=lambda x: x.uid):
+            if not u.active or u.retired:
+                continue
+            while queue:
+                s = u.free_slot()
+                if s < 0:
+                    break
+                r = queue.popleft()
+                r.unit, r.slot, r.kv_len, r.needs_prefill = u.uid, s, 0, True
+                u.busy[s] = r
+
+    def _mode_switch(self, now):
+        switched_nodes = []
+        for u in sorted(self.units.values(), key=lambda x: x.uid):
+            if u.kind != "pipeline" or u.retired:
+                continue
+            u.retired = True
+            inflight = [u.busy[s] for s in sorted(u.busy)]
+            plan = plan_mode_switch(u.pipeline, [(r.rid, len(r.out)) for r in inflight],
+                                    self.prefill_ms_per_token)
+            locals_by_node = {n: self._local_unit(n) for n in u.nodes}
+            by_id = {r.rid: r for r in inflight}
+            for row in plan.assignments:
+                r = by_id[row.request_id]
+                tgt = locals_by_node[row.node]
+                s = tgt.free_slot()
+                r.unit, r.slot, r.kv_len, r.needs_prefill = tgt.uid, s, 0, True   # KV recompute
+                tgt.busy[s] = r
+            switched_nodes.extend(u.nodes)
+        if switched_nodes:
+            self.log(now, "mode_switch", model=self.cfg.name, nodes=sorted(switched_nodes), mode="local")
+        self.switched = True
+
+    def _step_unit(self, u):
+        """Enqueue one iteration for unit u; returns [(request, token_tensor, row)]."""
+        reqs = [u.busy[s] for s in sorted(u.busy)]
+        if not reqs:
+            return None
+        tokens, pos, seq, last = [], [], [], []
+        for r in reqs:
+            if r.needs_prefill:
+                ctx = r.prompt + r.out
+                tokens += ctx
+                pos += list(range(len(ctx)))
+                seq += [r.slot] * len(ctx)
+            else:
+                tokens.append(r.out[-1])
+                pos.append(r.kv_len)
+                seq.append(r.slot)
+            last.append(len(tokens) - 1)
+        tok = self._forward(u, tokens, pos, seq, last)
+        return reqs, tok
+
+    def run(self, trace, prompts: dict, mc_streams: dict, push_ctas: int = 0, pull_ctas: int = 64,
+            timeout_s: float = 120.0):
+        """Launch the multicast, then serve ``trace`` (TraceRecords whose
+        arrival_s is relative to the launch).  Returns the event list."""
+        torch = self.torch
+        devs = sorted(set(st.device for u in self.units.values() for st in u.stages) |
+                      set(self.cluster.node_device(n) for n in self.receivers))
+        for d in devs:
+            torch.cuda.synchronize(d)
+        self.t0 = time.perf_counter()
+        epoch = self.cluster.launch_devices(mc_streams, push_ctas, pull_ctas)
+        self.log(0.0, "scale_out", model=self.cfg.name, nodes=list(self.plan.nodes),
+                 sources=list(self.plan.sources), strategy="lambda_scale")
+        self.log(0.0, "allocation", allocated_gpus=len(self.receivers))
+        pending = deque(sorted(trace, key=lambda r: (r.arrival_s, r.request_id)))
+        queue = deque()
+        live = {}
+        tokens_emitted = 0
+        while True:
+            now = time.perf_counter() - self.t0
+            if now > timeout_s:
+                raise TimeoutError("serving loop exceeded its timeout")
+            while pending and pending[0].arrival_s <= now:
+                rec = pending.popleft()
+                r = Request(rec, list(prompts[rec.request_id]))
+                live[rec.request_id] = r
+                queue.append(r)
+                self.log(rec.arrival_s, "request_arrival", request=rec.request_id, model=rec.model_id)
+            if not self.switched:
+                done = self.cluster.complete_nodes(epoch)
+                now = time.perf_counter() - self.t0
+                for n in self.receivers:
+                    if n not in self.block_complete_s and all(done[n]):
+                        self.block_complete_s[n] = now
+                for u in self.units.values():
+                    if u.kind == "pipeline" and not u.active and not u.retired:
+                        if all(all(done[st.node][b] for b in range(st.block_lo, st.block_hi + 1))
+                               for st in u.stages):
+                            u.active = True
+                all_done = all(all(done[n]) for n in self.receivers)
+                if all_done and tokens_emitted >= self.switch_hold_tokens:
+                    self._mode_switch(now)
+            self._admit(queue)
+            work = []
+            for u in sorted(self.units.values(), key=lambda x: x.uid):
+                if u.active and not u.retired and u.busy:
+                    w = self._step_unit(u)
+                    if w:
+                        work.append((u, w))
+            if not work:
+                if not pending and not queue and all(r.done for r in live.values()) and self.switched:
+                    break
+                time.sleep(0.0002)
+                continue
+            host = [(u, reqs, tok.cpu()) for u, (reqs, tok) in work]   # syncs every unit's vocab device
+            now = time.perf_counter() - self.t0
+            for u, reqs, tok in host:
+                for r, t in zip(reqs, tok.tolist()):
+                    if r.needs_prefill:
+                        r.kv_len = len(r.prompt) + len(r.out)
+                        r.needs_prefill = False
+                    else:
+                        r.kv_len += 1
+                    r.out.append(int(t))
+                    tokens_emitted += 1
+                    if r.first_token_s is None:
+                        r.first_token_s = now
+                    self.log(now, "token_emitted", request=r.rid, node=u.emit_node, cold_capacity=u.cold)
+                    if r.done:
+                        r.done_s = now
+                        del u.busy[r.slot]
+                        self.log(now, "request_done", request=r.rid, node=u.emit_node)
+        self.cluster.wait_devices()
+        for d in devs:
+            torch.cuda.synchronize(d)
+        self.requests = live
+        return self.events
