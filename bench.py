@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pull-ctas", type=int, default=64)
     ap.add_argument("--no-gpu-source", action="store_true")
+    ap.add_argument("--no-serving", action="store_true")
+    ap.add_argument("--requests", type=int, default=16)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -274,6 +276,25 @@ def main():
         so2.close()
     so.close()
 
+    # --- execute-while-load serving (tokens/s + TTFT during load) ------------
+    serving = None
+    if distributed and N >= 3 and not args.no_serving:
+        torch.cuda.synchronize()
+        # CPU (gloo) barrier: an NCCL barrier would leave a spinning kernel on
+        # every idle rank's GPU and time-slice against rank 0's serving work
+        cpu_group = dist.new_group(backend="gloo")
+        dist.barrier(group=cpu_group)       # every rank has freed its images
+        if rank == 0:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from serve_bench import run_serving
+            try:
+                serving = run_serving(N, model=C2_MODEL, k=2, blocks=C2_BLOCKS, requests=args.requests)
+                serving["note"] = ("rank 0 drives all N GPUs from one process for this sub-measurement "
+                                   "(cross-device pipelines); other ranks idle at a barrier")
+            except Exception as e:  # noqa: BLE001
+                serving = {"error": f"{type(e).__name__}: {e}"}
+        dist.barrier(group=cpu_group)
+
     if rank == 0:
         threads = os.cpu_count() or 1
         cpu = None
@@ -313,6 +334,8 @@ def main():
         }
         if gpu_source:
             line["gpu_source"] = gpu_source
+        if serving:
+            line["execute_while_load"] = serving
         print(json.dumps(line), flush=True)
     if distributed:
         dist.barrier()

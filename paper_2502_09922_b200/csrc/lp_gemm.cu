@@ -286,10 +286,12 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
   if (make_map(&mw, W, N, K, BM) != 0) return -1;
   if (make_map(&mw2, EPI == EPI_SWIGLU ? W2 : W, N, K, BM) != 0) return -1;
   if (make_map(&mx, X, T, K, BT) != 0) return -1;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;   // per-device bit: the smem opt-in is a per-device function attribute
+  int dev = 0;
+  LP_CUDA(cudaGetDevice(&dev));
+  if (!(attr_set >> dev & 1)) {
     LP_CUDA(cudaFuncSetAttribute(gemm_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_set = true;
+    attr_set |= 1ull << dev;
   }
   GemmArgs a;
   a.out = out;

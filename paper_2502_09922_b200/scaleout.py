@@ -72,6 +72,23 @@ def plan_scale_out(config, n_nodes: int, k: int = 1, block_count="auto",
     return ScaleOutPlan(cfg, layout, nodes, sources, groups, sched, ordered, eps, step_s, host_source)
 
 
+def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
+    """Transfers executed by ``node`` — the host-side mirror of the engine's
+    op assignment (lp_multicast.cu compile()): the receiver executes when
+    direction == 1 (pull) or the sender is the HOST node, else the sender.
+    Rows (step, sender, receiver, block, wait) in (step, sender, receiver)
+    order; ``wait`` = the sender is not a source (it must first receive)."""
+    host = 0 if plan.host_source else None
+    srcs = set(plan.sources)
+    rows = sorted((t.step, t.sender, t.receiver, t.block_id) for row in plan.schedule.steps for t in row)
+    out = []
+    for step, snd, rcv, blk in rows:
+        pulled = direction == 1 or snd == host
+        if (pulled and rcv == node) or (not pulled and snd == node):
+            out.append((step, snd, rcv, blk, int(snd not in srcs)))
+    return out
+
+
 @dataclass
 class ScaleOutResult:
     epoch: int
