@@ -108,11 +108,13 @@ int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch,
  * op's next tile is not ready yet. */
 int lp_mc_configure(lp_mc* mc, int direction, int push_mode, int pull_mode, int64_t chunk_bytes,
                     int window);
-/* Copy-engine executor for one GPU node (direction 1 only): enqueue, on the
- * node's `n_streams` streams, every transfer it receives as per-tile
- * cuStreamWaitValue32(sender flag) -> cudaMemcpyAsync -> cuStreamWriteValue32
- * (own flag); no SM work.  block_events (optional, n_blocks entries, NULL to
- * skip) are recorded after each received block's last tile. */
+/* Copy-engine executor for one GPU node: enqueue, on the node's `n_streams`
+ * streams, its ops as per-tile cuStreamWaitValue32(sender's flag) ->
+ * cudaMemcpyAsync -> cuStreamWriteValue32(receiver's flag); no SM work.
+ * direction 1 (lp_mc_configure): pulls everything it receives; direction 0:
+ * pushes everything it sends (waits on its own flags) and pulls host-sourced
+ * blocks.  block_events (optional, n_blocks entries, NULL to skip) are
+ * recorded after each pulled block's last tile. */
 int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
                  void* const* block_events);
 /* synchronise `stream`; code = 1 (and return -3) if a flag wait timed out */

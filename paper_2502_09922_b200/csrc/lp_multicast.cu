@@ -671,38 +671,47 @@ int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const
   if (resolve_stream_memops() != 0) return -1;
   LP_CHECK(mc && node >= 0 && node < mc->n_nodes, "lp_mc_run_ce: bad node");
   LP_CHECK(epoch >= 1 && n_streams >= 1 && streams, "lp_mc_run_ce: bad arguments");
-  LP_CHECK(mc->direction == 1, "lp_mc_run_ce: copy-engine execution is receiver-driven (direction 1)");
   LP_CHECK(mc->nodes[node].kind == LP_NODE_GPU, "lp_mc_run_ce: node %d is not a GPU node", node);
   if (mc->dirty && compile(mc) != 0) return -2;
   const ExecDesc ex = mc->per_node[node];
-  const NodeDev me = mc->nodes[node];
-  for (int oi = ex.pull_b; oi < ex.pull_e; ++oi) {
-    const OpDev op = mc->h_ops[oi];
-    const BlockDev bl = mc->blocks[op.block];
-    const NodeDev src = mc->nodes[op.src];
-    CUstream s = (CUstream)streams[(oi - ex.pull_b) % n_streams];
-    for (int t = 0; t < bl.ntiles; ++t) {
-      const int64_t lo = (int64_t)t * mc->tile_bytes;
-      const int64_t n = std::min<int64_t>(mc->tile_bytes, bl.len - lo);
-      if (op.wait) {
-        CUresult r = cuStreamWaitValue32(s, (CUdeviceptr)(src.flags + bl.tile_base + t), epoch,
-                                         CU_STREAM_WAIT_VALUE_GEQ);
-        LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWaitValue32 failed (%d)", (int)r);
+  // direction 1: this node's copy engine pulls every block it receives;
+  // direction 0: its copy engine pushes every block it sends (waits are then
+  // on its OWN flags, flag writes land in the receiver's memory) and it still
+  // pulls host-sourced blocks.  Both run in schedule step order.
+  int k = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int ob = pass == 0 ? ex.push_b : ex.pull_b;
+    const int oe = pass == 0 ? ex.push_e : ex.pull_e;
+    for (int oi = ob; oi < oe; ++oi, ++k) {
+      const OpDev op = mc->h_ops[oi];
+      const BlockDev bl = mc->blocks[op.block];
+      const NodeDev src = mc->nodes[op.src];
+      const NodeDev dst = mc->nodes[op.dst];
+      CUstream s = (CUstream)streams[k % n_streams];
+      for (int t = 0; t < bl.ntiles; ++t) {
+        const int64_t lo = (int64_t)t * mc->tile_bytes;
+        const int64_t n = std::min<int64_t>(mc->tile_bytes, bl.len - lo);
+        if (op.wait) {
+          CUresult r = cuStreamWaitValue32(s, (CUdeviceptr)(src.flags + bl.tile_base + t), epoch,
+                                           CU_STREAM_WAIT_VALUE_GEQ);
+          LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWaitValue32 failed (%d)", (int)r);
+        }
+        LP_CUDA(cudaMemcpyAsync(dst.image + bl.off + lo, src.image + bl.off + lo, (size_t)n, cudaMemcpyDefault,
+                                (cudaStream_t)s));
+        CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.flags + bl.tile_base + t), epoch,
+                                          CU_STREAM_WRITE_VALUE_DEFAULT);
+        LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
       }
-      LP_CUDA(cudaMemcpyAsync(me.image + bl.off + lo, src.image + bl.off + lo, (size_t)n, cudaMemcpyDefault,
-                              (cudaStream_t)s));
-      CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(me.flags + bl.tile_base + t), epoch,
+      CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.counts + op.block), epoch * (uint32_t)bl.ntiles,
                                         CU_STREAM_WRITE_VALUE_DEFAULT);
       LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
+      if (dst.ready) {
+        r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.ready + op.block), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+        LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: ready write failed (%d)", (int)r);
+      }
+      if (block_events && block_events[op.block] && pass == 1)
+        LP_CUDA(cudaEventRecord((cudaEvent_t)block_events[op.block], (cudaStream_t)s));
     }
-    CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(me.counts + op.block), epoch * (uint32_t)bl.ntiles,
-                                      CU_STREAM_WRITE_VALUE_DEFAULT);
-    LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
-    if (me.ready) {
-      r = cuStreamWriteValue32(s, (CUdeviceptr)(me.ready + op.block), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
-      LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: ready write failed (%d)", (int)r);
-    }
-    if (block_events && block_events[op.block]) LP_CUDA(cudaEventRecord((cudaEvent_t)block_events[op.block], (cudaStream_t)s));
   }
   return 0;
 }

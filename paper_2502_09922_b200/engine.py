@@ -445,7 +445,7 @@ class Cluster:
         """Make ``stream`` wait for every CE stream of this process."""
         import torch
         for node in self.exec_nodes:
-            for st in self.ce_streams(node):
+            for st in getattr(self, "_ce", {}).get(node, []):
                 ev = torch.cuda.Event()
                 ev.record(st)
                 stream.wait_event(ev)

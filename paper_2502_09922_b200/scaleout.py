@@ -118,7 +118,7 @@ class ScaleOut:
             raise ValueError("executor is 'kernel' (in-kernel NVLink/PCIe copies) or 'ce' (copy engines)")
         self.executor = executor
         self.ce_streams = ce_streams
-        self.cluster.engine.configure(1 if executor == "ce" else direction, copy_mode, copy_mode, chunk_bytes, 3)
+        self.cluster.engine.configure(direction, copy_mode, copy_mode, chunk_bytes, 3)
         self.seed = seed
         self.device = device
         self._loaded = False

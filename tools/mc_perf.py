@@ -52,10 +52,10 @@ def main():
     results = []
     for tile in [int(x) for x in a.tile.split(",")]:
         so = SO.ScaleOut(plan, distributed=a.dist, tile_bytes=tile, device=torch.cuda.current_device(),
-                         executor=a.executor, ce_streams=a.ce_streams)
+                         executor=a.executor, ce_streams=a.ce_streams, direction=a.direction)
         so.load_sources()
         for chunk, window in [(int(c), int(w)) for c in a.chunk.split(",") for w in a.window.split(",")]:
-          so.cluster.engine.configure(1 if a.executor == "ce" else a.direction, a.push_mode, a.pull_mode, chunk, window)
+          so.cluster.engine.configure(a.direction, a.push_mode, a.pull_mode, chunk, window)
           for push in [int(x) for x in a.push.split(",")]:
             for pull in [int(x) for x in a.pull.split(",")]:
                 so.push_ctas, so.pull_ctas = push, pull
