@@ -36,6 +36,15 @@ def _vp(x):
     return C.c_void_p(x if isinstance(x, int) else x.data_ptr())
 
 
+def _cur_stream(stream):
+    """Kernels go to torch's current stream unless told otherwise (so they
+    are captured by ``torch.cuda.graph``)."""
+    if stream is not None:
+        return stream
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
 class KVCache:
     """bf16 K and V caches per layer: [max_seqs, n_kv, max_len, head_dim]."""
 
@@ -61,8 +70,10 @@ class LlamaExecutor:
         self.layer_hi = self.cfg.n_layers - 1 if layer_hi is None else layer_hi
         self.vocab_ops = vocab_ops
         self.torch_device = torch.device(f"cuda:{device}")
-        self.cache = KVCache(self.cfg, range(self.layer_lo, self.layer_hi + 1), max_seqs, max_len,
+        # one extra sequence slot: scratch for padded rows of captured decode graphs
+        self.cache = KVCache(self.cfg, range(self.layer_lo, self.layer_hi + 1), max_seqs + 1, max_len,
                              self.torch_device)
+        self.scratch_seq = max_seqs
         self.lib = N.lib()
 
     # -- weights ----------------------------------------------------------------
@@ -82,7 +93,8 @@ class LlamaExecutor:
         N.check(self.lib.lp_gemm_bf16(C.c_void_p(w), n_rows, k, _vp(x), tokens, _vp(out), ldo, 0, split,
                                       C.c_void_p(stream)), "lp_gemm_bf16")
 
-    def embed(self, tokens, stream: int = 0):
+    def embed(self, tokens, stream=None):
+        stream = _cur_stream(stream)
         import torch
         T = tokens.numel()
         x = torch.empty((T, self.cfg.d_model), dtype=torch.float32, device=self.torch_device)
@@ -90,7 +102,8 @@ class LlamaExecutor:
                                   C.c_void_p(stream)), "lp_embed")
         return x
 
-    def layer(self, l: int, x, pos, seq, stream: int = 0):
+    def layer(self, l: int, x, pos, seq, stream=None):
+        stream = _cur_stream(stream)
         import torch
         cfg = self.cfg
         T, d = x.shape
@@ -121,8 +134,9 @@ class LlamaExecutor:
         self._gemm_add(self.ptr(f"layers.{l}.w_down"), d, cfg.ffn, act, T, x, d, stream)
         return x
 
-    def head(self, x, stream: int = 0):
+    def head(self, x, stream=None):
         """Final norm + LM head -> fp32 logits [T, V]."""
+        stream = _cur_stream(stream)
         import torch
         cfg = self.cfg
         T, d = x.shape
@@ -134,7 +148,8 @@ class LlamaExecutor:
                                       cfg.vocab, 1, 1, C.c_void_p(stream)), "lp_gemm_bf16")
         return logits
 
-    def greedy(self, logits, stream: int = 0):
+    def greedy(self, logits, stream=None):
+        stream = _cur_stream(stream)
         import torch
         T = logits.shape[0]
         tok = torch.empty((T,), dtype=torch.int32, device=self.torch_device)
@@ -143,7 +158,7 @@ class LlamaExecutor:
                 "lp_argmax")
         return tok, top2
 
-    def forward(self, tokens=None, x=None, pos=None, seq=None, stream: int = 0, want_logits: bool = True):
+    def forward(self, tokens=None, x=None, pos=None, seq=None, stream=None, want_logits: bool = True):
         """Embed (if tokens) -> layers [lo, hi] -> head (if this stage owns it)."""
         if x is None:
             x = self.embed(tokens, stream)
@@ -152,3 +167,66 @@ class LlamaExecutor:
         if want_logits and self.vocab_ops and self.layer_hi == self.cfg.n_layers - 1:
             return x, self.head(x, stream)
         return x, None
+
+
+class DecodeGraph:
+    """A CUDA graph of one batched decode step (embed -> all layers -> head ->
+    argmax) for a full-model executor, ``batch`` rows wide.  Rows past the
+    live batch are padded onto the executor's scratch sequence slot, so a
+    fixed-shape graph serves any batch <= ``batch``; one replay replaces
+    ~10 kernel launches per layer."""
+
+    def __init__(self, ex: LlamaExecutor, batch: int):
+        import torch
+        self.ex, self.batch = ex, batch
+        dev = ex.torch_device
+        self.tokens = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.pos = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.seq = torch.full((batch,), ex.scratch_seq, dtype=torch.int32, device=dev)
+        self.graph = None
+        self.out = None
+        # pinned staging: one H2D copy of [tokens | pos | seq], one D2H of the result
+        self.h_in = torch.zeros(3 * batch, dtype=torch.int32).pin_memory()
+        self.d_in = torch.zeros(3 * batch, dtype=torch.int32, device=dev)
+        self.h_out = torch.zeros(batch, dtype=torch.int32).pin_memory()
+
+    def _body(self):
+        b = self.batch
+        self.tokens.copy_(self.d_in[:b])
+        self.pos.copy_(self.d_in[b:2 * b])
+        self.seq.copy_(self.d_in[2 * b:])
+        _, logits = self.ex.forward(tokens=self.tokens, pos=self.pos, seq=self.seq)
+        tok, _ = self.ex.greedy(logits)
+        return tok
+
+    def capture(self):
+        import torch
+        with torch.cuda.device(self.ex.device):
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self._body()                      # warm-up: tensor maps, attributes, allocator
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = torch.cuda.CUDAGraph()
+            # explicit per-device capture stream: torch.cuda.graph's default side
+            # stream is created once, on whichever device captured first
+            with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(device=self.ex.device)):
+                self.out = self._body()
+
+    def step(self, tokens, pos, seq):
+        """Decode one token for each live row; returns the int32 device tensor."""
+        import torch
+        n = len(tokens)
+        if n > self.batch:
+            raise ValueError("batch larger than the captured graph")
+        if self.graph is None:
+            self.capture()
+        b = self.batch
+        pad = b - n
+        vals = list(tokens) + [0] * pad + list(pos) + [0] * pad + list(seq) + [self.ex.scratch_seq] * pad
+        self.h_in.numpy()[:] = vals
+        with torch.cuda.device(self.ex.device):
+            self.d_in.copy_(self.h_in, non_blocking=True)
+            self.graph.replay()
+            self.h_out.copy_(self.out, non_blocking=True)
+        return self.h_out[:n]

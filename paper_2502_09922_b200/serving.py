@@ -82,6 +82,7 @@ class Unit:
     active: bool = False
     retired: bool = False
     busy: dict = field(default_factory=dict)   # slot -> Request
+    graph: object = None                        # DecodeGraph (local units)
 
     @property
     def nodes(self) -> tuple:
@@ -102,7 +103,7 @@ class Server:
     """Serves a request trace while ``plan`` is being multicast."""
 
     def __init__(self, plan, cluster, local_slots: int = 8, max_len: int = 512, switch_hold_tokens: int = 0,
-                 prefill_ms_per_token: float = 0.5):
+                 prefill_ms_per_token: float = 0.5, use_graphs: bool = True):
         import torch
         self.plan = plan
         self.cluster = cluster
@@ -111,8 +112,10 @@ class Server:
         self.local_slots = local_slots
         self.max_len = max_len
         self.switch_hold_tokens = switch_hold_tokens
+        self.use_graphs = use_graphs
         self.prefill_ms_per_token = prefill_ms_per_token
         self.events = []
+        self.profile = []          # per iteration: (start, enqueue s, device s, tokens, unit batches)
         self.units = {}
         self._next_uid = 0
         self.switched = False
@@ -134,6 +137,9 @@ class Server:
                 stages.append(Stage(st.node, cluster.node_device(st.node), st.block_lo, st.block_hi, l_lo, l_hi,
                                     st.block_lo == 0))
             self._add_unit("pipeline", stages, max(1, len(ep.stages)), True, ep)
+        # post-switch local replicas, built (and their decode graphs captured)
+        # before the scale-out starts; activated at mode switch
+        self.local_units = {n: self._local_unit(n, active=False) for n in self.receivers}
 
     # -- units -------------------------------------------------------------------
     def _add_unit(self, kind, stages, slots, cold, pipeline=None):
@@ -147,11 +153,11 @@ class Server:
         self._next_uid += 1
         return u
 
-    def _local_unit(self, node):
+    def _local_unit(self, node, active: bool = True):
         dev = self.cluster.node_device(node)
         st = Stage(node, dev, 0, self.lay.plan.block_count - 1, 0, self.cfg.n_layers - 1, True)
         u = self._add_unit("local", [st], self.local_slots, True)
-        u.active = True
+        u.active = active
         return u
 
     def log(self, t, kind, **payload):
@@ -225,7 +231,9 @@ class Server:
             inflight = [u.busy[s] for s in sorted(u.busy)]
             plan = plan_mode_switch(u.pipeline, [(r.rid, len(r.out)) for r in inflight],
                                     self.prefill_ms_per_token)
-            locals_by_node = {n: self._local_unit(n) for n in u.nodes}
+            locals_by_node = {n: self.local_units[n] for n in u.nodes}
+            for lu in locals_by_node.values():
+                lu.active = True
             by_id = {r.rid: r for r in inflight}
             for row in plan.assignments:
                 r = by_id[row.request_id]
@@ -239,10 +247,26 @@ class Server:
         self.switched = True
 
     def _step_unit(self, u):
-        """Enqueue one iteration for unit u; returns [(request, token_tensor, row)]."""
+        """Enqueue one iteration for unit u; returns [(requests, token tensor)].
+
+        Local replicas decode through a captured CUDA graph (one replay per
+        step); prefills and pipeline units run eagerly."""
         reqs = [u.busy[s] for s in sorted(u.busy)]
         if not reqs:
             return None
+        out = []
+        if u.kind == "local" and self.use_graphs:
+            dec = [r for r in reqs if not r.needs_prefill]
+            reqs = [r for r in reqs if r.needs_prefill]
+            if dec:
+                if u.graph is None:
+                    from .llama import DecodeGraph
+                    u.graph = DecodeGraph(u.stages[0].executor, u.slots)
+                with self.torch.cuda.device(u.stages[0].device):
+                    tok = u.graph.step([r.out[-1] for r in dec], [r.kv_len for r in dec], [r.slot for r in dec])
+                out.append((dec, tok))
+            if not reqs:
+                return out
         tokens, pos, seq, last = [], [], [], []
         for r in reqs:
             if r.needs_prefill:
@@ -256,7 +280,22 @@ class Server:
                 seq.append(r.slot)
             last.append(len(tokens) - 1)
         tok = self._forward(u, tokens, pos, seq, last)
-        return reqs, tok
+        out.append((reqs, tok))
+        return out
+
+    def _warm_up(self, tokens: int = 16):
+        """One dummy ragged forward per unit on its scratch sequence slot
+        before the clock starts: loads every kernel module on every device and
+        sets the per-device smem attributes, so the first real request does
+        not pay them.  Receiver weights are still garbage here — harmless, only
+        the scratch KV slot is written."""
+        torch = self.torch
+        for u in self.units.values():
+            scratch = u.stages[0].executor.scratch_seq
+            n = min(tokens, self.max_len)
+            self._forward(u, [0] * n, list(range(n)), [scratch] * n, [n - 1])
+        for d in {st.device for u in self.units.values() for st in u.stages}:
+            torch.cuda.synchronize(d)
 
     def run(self, trace, prompts: dict, mc_streams: dict, push_ctas: int = 0, pull_ctas: int = 64,
             timeout_s: float = 120.0):
@@ -265,6 +304,13 @@ class Server:
         torch = self.torch
         devs = sorted(set(st.device for u in self.units.values() for st in u.stages) |
                       set(self.cluster.node_device(n) for n in self.receivers))
+        self._warm_up()
+        if self.use_graphs:
+            from .llama import DecodeGraph
+            for u in self.local_units.values():
+                if u.graph is None:
+                    u.graph = DecodeGraph(u.stages[0].executor, u.slots)
+                    u.graph.capture()
         for d in devs:
             torch.cuda.synchronize(d)
         self.t0 = time.perf_counter()
@@ -301,18 +347,24 @@ class Server:
                 if all_done and tokens_emitted >= self.switch_hold_tokens:
                     self._mode_switch(now)
             self._admit(queue)
+            t_enq = time.perf_counter()
             work = []
             for u in sorted(self.units.values(), key=lambda x: x.uid):
                 if u.active and not u.retired and u.busy:
-                    w = self._step_unit(u)
-                    if w:
+                    for w in self._step_unit(u) or []:
                         work.append((u, w))
             if not work:
                 if not pending and not queue and all(r.done for r in live.values()) and self.switched:
                     break
                 time.sleep(0.0002)
                 continue
-            host = [(u, reqs, tok.cpu()) for u, (reqs, tok) in work]   # syncs every unit's vocab device
+            t_sync = time.perf_counter()
+            for d in {u.stages[0].device for u, _ in work} | {st.device for u, _ in work for st in u.stages}:
+                torch.cuda.synchronize(d)
+            t_done = time.perf_counter()
+            self.profile.append((t_enq - self.t0, t_sync - t_enq, t_done - t_sync,
+                                 sum(len(w[0]) for _, w in work), sum(1 for _, w in work)))
+            host = [(u, reqs, tok.cpu()) for u, (reqs, tok) in work]
             now = time.perf_counter() - self.t0
             for u, reqs, tok in host:
                 for r, t in zip(reqs, tok.tolist()):

@@ -36,7 +36,8 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         cl.set_schedule_all(plan.schedule, plan.sources)
         for d in range(n_gpus):
             cl.per_device[d].configure(1, 0, 0, 16384, 3)
-        srv = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8)
+        graphs = not os.environ.get("LP_NO_GRAPHS")
+        srv = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs)
         rng = np.random.default_rng(seed)
         prompts = {f"r{i}": rng.integers(0, plan.config.vocab, prompt_len).tolist() for i in range(requests)}
         trace = [TraceRecord(f"r{i}", spacing_s * i, model, prompt_len, out_tokens) for i in range(requests)]
@@ -44,7 +45,7 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         # warm-up (kernels, allocator, tensor maps): a tiny burst on a second epoch is not needed;
         # run one short pass first and report the second
         srv.run(trace[:2], prompts, streams, pull_ctas=pull_ctas)
-        srv2 = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8)
+        srv2 = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs)
         ev = srv2.run(trace, prompts, streams, pull_ctas=pull_ctas)
         rep = aggregate(ev, "lambda_scale")
         first_full = min(srv2.block_complete_s.values()) if srv2.block_complete_s else None
@@ -52,6 +53,21 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         t_switch = next((e.time_s for e in ev if e.kind == "mode_switch"), None)
         pipe_tokens = sum(1 for e in ev if e.kind == "token_emitted" and (t_switch is None or e.time_s < t_switch))
         busy = [x for x in rep.throughput_timeline if x[1] > 0]
+        if os.environ.get("LP_SERVE_PROFILE"):
+            import time as _t
+            for n, u in srv2.local_units.items():
+                if u.graph is None:
+                    continue
+                d = u.stages[0].device
+                with torch.cuda.device(d):
+                    torch.cuda.synchronize(d)
+                    t0 = _t.perf_counter()
+                    for _ in range(5):
+                        u.graph.graph.replay()
+                    torch.cuda.synchronize(d)
+                    print(f"replay node {n} dev {d}: {(_t.perf_counter() - t0) / 5 * 1e3:.2f} ms", file=sys.stderr)
+            for row in srv2.profile:
+                print("iter t=%.4f enq=%.4f dev=%.4f tokens=%d batches=%d" % row, file=sys.stderr)
         return {
             "workload": f"{model} bf16, GPU sources {plan.sources}, receivers {plan.receivers}, b={blocks}, k={k}; "
                         f"{requests} requests x (prompt {prompt_len}, out {out_tokens}), {spacing_s * 1e3:.0f} ms apart at t=0",
