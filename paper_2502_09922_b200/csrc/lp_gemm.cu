@@ -112,6 +112,9 @@ struct Cfg {
   static constexpr int B_BYTES = BT * BK * 2;
   static constexpr int NA = (EPI == EPI_SWIGLU) ? 2 : 1;   // weight tiles per stage
   static constexpr int STAGE_BYTES = NA * A_BYTES + B_BYTES;
+  // <= 6 stages: small decode tiles (18-34 KiB/stage) then fit two CTAs per SM,
+  // which overlaps one CTA's prologue/epilogue with the other's streaming —
+  // measured faster than a single 12-stage CTA (profiles/gemm_split_sweep_r01.txt)
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
   static constexpr int ACC_COLS = NA * BT;
   static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128

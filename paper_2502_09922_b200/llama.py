@@ -89,7 +89,9 @@ class LlamaExecutor:
     # -- kernels ------------------------------------------------------------------
     def _gemm_add(self, w: int, n_rows: int, k: int, x, tokens: int, out, ldo: int, stream: int):
         tiles = -(-n_rows // 128) * -(-tokens // 128)
-        split = max(1, min(_SMS // max(tiles, 1), max(1, (k // 64) // 4)))
+        # ~160 CTAs (just over one wave of 148 SMs) measured best for decode
+        # shapes (profiles/gemm_split_sweep_r01.txt); keep >= 4 k-blocks per split
+        split = max(1, min(round(160 / max(tiles, 1)), max(1, (k // 64) // 4)))
         N.check(self.lib.lp_gemm_bf16(C.c_void_p(w), n_rows, k, _vp(x), tokens, _vp(out), ldo, 0, split,
                                       C.c_void_p(stream)), "lp_gemm_bf16")
 
