@@ -260,20 +260,34 @@ def main():
     gpu_source = None
     if distributed and N >= 2 and not args.no_gpu_source:
         plan2 = SO.plan_scale_out(C2_MODEL, N, 1, C2_BLOCKS)
-        so2 = SO.ScaleOut(plan2, distributed=True, tile_bytes=2 << 20, push_ctas=0, pull_ctas=64,
-                          seed=SEED, device=dev, direction=1, copy_mode=0)
-        so2.load_sources()
-        t2 = timed_steps(so2, args.steps, args.warmup, True, stream)
-        T2 = statistics.median(t2)
         M2 = plan2.layout.weights_bytes
         src_egress = sum(plan2.layout.block_lengths[int(ln.split(",")[3])] for ln in plan2.lines()
                          if int(ln.split(",")[1]) == 0)
         gpu_source = {"workload": f"{C2_MODEL} bf16 GPU0->{N - 1} peers, b={C2_BLOCKS}, k=1",
-                      "ms": round(T2, 3), "agg_GBps": round((N - 1) * M2 / (T2 * 1e-3) / 1e9, 1),
-                      "nvlink_roofline_frac": round(M2 / (900e9 * T2 * 1e-3), 4),
-                      "schedule_ceiling": round(M2 / src_egress, 4),
-                      "executor": "in-kernel NVLink pulls (LDG.128, 64 CTAs/rank, 2 MiB tiles)"}
-        so2.close()
+                      "schedule_ceiling": round(M2 / src_egress, 4), "executors": {}}
+        for name, kw in (("kernel", dict(executor="kernel", tile_bytes=2 << 20, pull_ctas=64, copy_mode=0)),
+                         ("copy_engine", dict(executor="ce", tile_bytes=SO.CE_TILE))):
+            so2 = SO.ScaleOut(plan2, distributed=True, push_ctas=0, seed=SEED, device=dev, direction=1, **kw)
+            so2.load_sources()
+            t2 = timed_steps(so2, args.steps, args.warmup, True, stream)
+            T2 = statistics.median(t2)
+            sums = so2.checksums(so2.cluster.exec_nodes[0])
+            src = [None]
+            if rank == 0:
+                src = [so2.checksums(0)]
+            dist.broadcast_object_list(src, src=0)
+            exact = torch.tensor([int(sums == src[0])], device="cuda")
+            dist.all_reduce(exact, op=dist.ReduceOp.MIN)
+            gpu_source["executors"][name] = {
+                "ms": round(T2, 3), "agg_GBps": round((N - 1) * M2 / (T2 * 1e-3) / 1e9, 1),
+                "nvlink_roofline_frac": round(M2 / (900e9 * T2 * 1e-3), 4), "byte_exact": bool(exact.item()),
+                "detail": ("in-kernel NVLink pulls (LDG.128, 64 CTAs/rank, 2 MiB tiles)" if name == "kernel" else
+                           "copy engines: cuStreamWaitValue32 -> cudaMemcpyAsync -> cuStreamWriteValue32, "
+                           "256 MiB tiles, no SMs")}
+            so2.close()
+        best = min(gpu_source["executors"].items(), key=lambda kv: kv[1]["ms"])
+        gpu_source.update({"best_executor": best[0], "ms": best[1]["ms"], "agg_GBps": best[1]["agg_GBps"],
+                           "nvlink_roofline_frac": best[1]["nvlink_roofline_frac"]})
     so.close()
 
     # --- execute-while-load serving (tokens/s + TTFT during load) ------------

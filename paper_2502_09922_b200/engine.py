@@ -366,6 +366,20 @@ class Cluster:
             eng.run(mine, self.epoch, push_ctas, pull_ctas, streams[d])
         return self.epoch
 
+    def launch_devices_ce(self, streams: dict) -> int:
+        """Multi-device launch on copy engines: every GPU node's ops enqueued
+        on its device's stream (``streams``: device -> torch stream)."""
+        self.epoch += 1
+        self._mc_streams = {}
+        for d, eng in self.per_device.items():
+            N.call("lp_set_device", d)
+            st = streams[d]
+            ptr = st if isinstance(st, int) else st.cuda_stream
+            for nb in self.nodes:
+                if nb.kind == LP_NODE_GPU and nb.device == d:
+                    eng.run_ce(nb.node, self.epoch, [ptr])
+        return self.epoch
+
     def wait_devices(self) -> None:
         """Synchronise every per-device multicast launch; raise on a watchdog expiry."""
         for d, eng in getattr(self, "per_device", {}).items():

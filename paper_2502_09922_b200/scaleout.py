@@ -89,6 +89,20 @@ def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
     return out
 
 
+CE_TILE = 256 << 20
+
+
+def choose_executor(plan: ScaleOutPlan, tile_bytes: int = E.DEFAULT_TILE):
+    """Measured policy (profiles/mc_sweeps_r01.md, p2p_micro_r01.txt):
+    GPU-sourced schedules with relays (>= 3 nodes) run on the copy engines
+    with 256 MiB tiles — DMA keeps ~778 GB/s per direction while a relay
+    sends and receives, SM-issued NVLink traffic drops to ~673 GB/s —
+    everything else (host sources, 1 -> 1) runs in-kernel (2 MiB tiles)."""
+    if not plan.host_source and len(plan.nodes) >= 3:
+        return "ce", CE_TILE
+    return "kernel", tile_bytes
+
+
 @dataclass
 class ScaleOutResult:
     epoch: int
@@ -102,10 +116,12 @@ class ScaleOut:
 
     def __init__(self, plan: ScaleOutPlan, distributed: bool = False, tile_bytes: int = E.DEFAULT_TILE,
                  push_ctas: int = 0, pull_ctas: int = 64, seed: int = 0, device: int = 0, direction: int = 1,
-                 copy_mode: int = 1, chunk_bytes: int = 16384, executor: str = "kernel", ce_streams: int = 2):
+                 copy_mode: int = 1, chunk_bytes: int = 16384, executor: str = "kernel", ce_streams: int = 1):
         self.plan = plan
         self.distributed = distributed
         self.push_ctas, self.pull_ctas = push_ctas, pull_ctas
+        if executor == "auto":
+            executor, tile_bytes = choose_executor(plan, tile_bytes)
         lay = plan.layout
         if distributed:
             self.cluster = E.Cluster.distributed(lay.block_offsets, lay.block_lengths, lay.weights_bytes,
@@ -115,7 +131,7 @@ class ScaleOut:
             self.cluster = E.Cluster.local(n_gpu, lay.block_offsets, lay.block_lengths, lay.weights_bytes,
                                            device=device, host_node=plan.host_source, tile_bytes=tile_bytes)
         if executor not in ("kernel", "ce"):
-            raise ValueError("executor is 'kernel' (in-kernel NVLink/PCIe copies) or 'ce' (copy engines)")
+            raise ValueError("executor is 'kernel' (in-kernel NVLink/PCIe copies), 'ce' (copy engines) or 'auto'")
         self.executor = executor
         self.ce_streams = ce_streams
         self.cluster.engine.configure(direction, copy_mode, copy_mode, chunk_bytes, 3)

@@ -298,7 +298,7 @@ class Server:
             torch.cuda.synchronize(d)
 
     def run(self, trace, prompts: dict, mc_streams: dict, push_ctas: int = 0, pull_ctas: int = 64,
-            timeout_s: float = 120.0):
+            timeout_s: float = 120.0, executor: str = "kernel"):
         """Launch the multicast, then serve ``trace`` (TraceRecords whose
         arrival_s is relative to the launch).  Returns the event list."""
         torch = self.torch
@@ -314,7 +314,10 @@ class Server:
         for d in devs:
             torch.cuda.synchronize(d)
         self.t0 = time.perf_counter()
-        epoch = self.cluster.launch_devices(mc_streams, push_ctas, pull_ctas)
+        if executor == "ce":
+            epoch = self.cluster.launch_devices_ce(mc_streams)
+        else:
+            epoch = self.cluster.launch_devices(mc_streams, push_ctas, pull_ctas)
         self.log(0.0, "scale_out", model=self.cfg.name, nodes=list(self.plan.nodes),
                  sources=list(self.plan.sources), strategy="lambda_scale")
         self.log(0.0, "allocation", allocated_gpus=len(self.receivers))
@@ -382,7 +385,11 @@ class Server:
                         r.done_s = now
                         del u.busy[r.slot]
                         self.log(now, "request_done", request=r.rid, node=u.emit_node)
-        self.cluster.wait_devices()
+        if executor == "ce":
+            for st in mc_streams.values():
+                st.synchronize()
+        else:
+            self.cluster.wait_devices()
         for d in devs:
             torch.cuda.synchronize(d)
         self.requests = live

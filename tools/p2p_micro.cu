@@ -90,6 +90,11 @@ int main() {
   auto push = [&](int s, int d) { CK(cudaSetDevice(s)); vec_copy<8><<<C, 512, 0, st[s]>>>((const int4*)buf[s][0], (int4*)buf[d][1], bytes / 16); };
   auto ce = [&](int s, int d) { CK(cudaSetDevice(s)); CK(cudaMemcpyPeerAsync(buf[d][1], d, buf[s][0], s, bytes, st[s])); };
   auto tpull = [&](int d, int s, int c) { CK(cudaSetDevice(d)); CK(cudaFuncSetAttribute(tma_copy<12, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 16384)); tma_copy<12, 9><<<c, 32, 12 * 16384, st[d]>>>(buf[s][0], buf[d][1], bytes, 16384); };
+  auto cepull = [&](int d, int s) { CK(cudaSetDevice(d)); CK(cudaMemcpyPeerAsync(buf[d][1], d, buf[s][0], s, bytes, st[d])); };
+  run("CE pull 1<-0 alone (stream on dst)", [&] { cepull(1, 0); });
+  run("CE pull chain 1<-0, 2<-1", [&] { cepull(1, 0); cepull(2, 1); });
+  run("mixed: CE pull 1<-0 + SM pull 2<-1", [&] { cepull(1, 0); pull(2, 1); });
+  run("mixed: SM pull 1<-0 + CE pull 2<-1", [&] { pull(1, 0); cepull(2, 1); });
   run("CE 0->1 alone", [&] { ce(0, 1); });
   run("CE 0->1 and 1->0", [&] { ce(0, 1); ce(1, 0); });
   run("CE chain 0->1, 1->2", [&] { ce(0, 1); ce(1, 2); });

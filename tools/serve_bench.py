@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int = 16, requests: int = 16,
                 prompt_len: int = 128, out_tokens: int = 32, spacing_s: float = 0.001, pull_ctas: int = 32,
-                local_slots: int = 8, seed: int = 20250815):
+                local_slots: int = 8, seed: int = 20250815, executor: str = "ce"):
     import numpy as np
     import torch
 
@@ -28,8 +28,9 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
 
     plan = SO.plan_scale_out(model, n_gpus, k=k, block_count=blocks)
     lay = plan.layout
+    tile = SO.CE_TILE if executor == "ce" else 2 << 20
     cl = E.Cluster.devices(list(range(n_gpus)), lay.block_offsets, lay.block_lengths, lay.weights_bytes,
-                           tile_bytes=2 << 20)
+                           tile_bytes=tile)
     try:
         for s in plan.sources:
             E.load_source_image(cl, s, lay, seed)
@@ -44,9 +45,9 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         streams = {d: torch.cuda.Stream(device=d) for d in range(n_gpus)}
         # warm-up (kernels, allocator, tensor maps): a tiny burst on a second epoch is not needed;
         # run one short pass first and report the second
-        srv.run(trace[:2], prompts, streams, pull_ctas=pull_ctas)
+        srv.run(trace[:2], prompts, streams, pull_ctas=pull_ctas, executor=executor)
         srv2 = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs)
-        ev = srv2.run(trace, prompts, streams, pull_ctas=pull_ctas)
+        ev = srv2.run(trace, prompts, streams, pull_ctas=pull_ctas, executor=executor)
         rep = aggregate(ev, "lambda_scale")
         first_full = min(srv2.block_complete_s.values()) if srv2.block_complete_s else None
         all_full = max(srv2.block_complete_s.values()) if srv2.block_complete_s else None
@@ -69,6 +70,7 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
             for row in srv2.profile:
                 print("iter t=%.4f enq=%.4f dev=%.4f tokens=%d batches=%d" % row, file=sys.stderr)
         return {
+            "multicast_executor": executor,
             "workload": f"{model} bf16, GPU sources {plan.sources}, receivers {plan.receivers}, b={blocks}, k={k}; "
                         f"{requests} requests x (prompt {prompt_len}, out {out_tokens}), {spacing_s * 1e3:.0f} ms apart at t=0",
             "pipelines": [[(st.node, st.block_lo, st.block_hi) for st in ep.stages] for ep in plan.pipelines],
