@@ -117,6 +117,9 @@ int lp_mc_configure(lp_mc* mc, int direction, int push_mode, int pull_mode, int6
  * recorded after each pulled block's last tile. */
 int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
                  void* const* block_events);
+/* tunables: "wide_loads" (0/1: 256 B L2 fetch granule on LDG-role loads),
+ * "window" (1..8), "timeout_ms" (flag-wait watchdog, default 20000) */
+int lp_mc_set_option(lp_mc* mc, const char* name, int64_t value);
 /* synchronise `stream`; code = 1 (and return -3) if a flag wait timed out */
 int lp_mc_status(lp_mc* mc, void* stream, int* code);
 /* zero a node's signal area (call on every node, then barrier, before epoch 1) */

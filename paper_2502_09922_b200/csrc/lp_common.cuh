@@ -65,6 +65,14 @@ __device__ __forceinline__ int4 ld_stream16(const int4* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+// same, with a 256-byte L2 fetch granule: remote (NVLink) and host (PCIe)
+// reads then go out as 256 B requests instead of 32-128 B sectors
+__device__ __forceinline__ int4 ld_stream16_l2_256(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.cg.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ void st16(int4* p, const int4& v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");

@@ -22,6 +22,7 @@
 #include "../../include/lambdapipe.h"
 #include <cuda.h>
 #include <algorithm>
+#include <string.h>
 #include <vector>
 
 #define LP_MAX_EXEC 32
@@ -63,6 +64,7 @@ struct McParams {
   int push_ctas, pull_ctas, n_exec;
   int push_mode, pull_mode;   // 0 = LDG/STG vectors, 1 = TMA bulk pipeline
   int window;                 // ops a CTA may interleave (ldg role)
+  int wide_loads;             // 256 B L2 fetch granule on LDG-role loads
   ExecDesc exec[LP_MAX_EXEC];
 };
 
@@ -81,7 +83,13 @@ __device__ __forceinline__ bool wait_flag(const uint32_t* f, uint32_t epoch, uin
   return true;
 }
 
-__device__ __forceinline__ void copy_tile(const char* __restrict__ s, char* __restrict__ d, int64_t n) {
+template <bool WIDE>
+__device__ __forceinline__ int4 ld16(const int4* p) {
+  return WIDE ? lp::ld_stream16_l2_256(p) : lp::ld_stream16(p);
+}
+
+template <bool WIDE>
+__device__ __forceinline__ void copy_tile_t(const char* __restrict__ s, char* __restrict__ d, int64_t n) {
   constexpr int U = 8;
   const int4* s4 = reinterpret_cast<const int4*>(s);
   int4* d4 = reinterpret_cast<int4*>(d);
@@ -91,11 +99,18 @@ __device__ __forceinline__ void copy_tile(const char* __restrict__ s, char* __re
   for (; i + (int64_t)(U - 1) * T < n16; i += (int64_t)U * T) {
     int4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = lp::ld_stream16(s4 + i + (int64_t)u * T);
+    for (int u = 0; u < U; ++u) v[u] = ld16<WIDE>(s4 + i + (int64_t)u * T);
 #pragma unroll
     for (int u = 0; u < U; ++u) lp::st16(d4 + i + (int64_t)u * T, v[u]);
   }
-  for (; i < n16; i += T) lp::st16(d4 + i, lp::ld_stream16(s4 + i));
+  for (; i < n16; i += T) lp::st16(d4 + i, ld16<WIDE>(s4 + i));
+}
+
+__device__ __forceinline__ void copy_tile(const char* __restrict__ s, char* __restrict__ d, int64_t n, bool wide) {
+  if (wide)
+    copy_tile_t<true>(s, d, n);
+  else
+    copy_tile_t<false>(s, d, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -174,7 +189,7 @@ __device__ void ldg_role(const McParams& p, int ob, int oe, int lane, int lanes,
     const NodeDev dst = p.nodes[op.dst];
     const int64_t lo = (int64_t)t * p.tile_bytes;
     const int64_t n = min(p.tile_bytes, bl.len - lo);
-    copy_tile(src.image + bl.off + lo, dst.image + bl.off + lo, n);
+    copy_tile(src.image + bl.off + lo, dst.image + bl.off + lo, n, p.wide_loads != 0);
     __syncthreads();  // every thread's stores of this tile precede the flag
     if (threadIdx.x == 0) {
       lp::fence_sys();
@@ -388,6 +403,8 @@ struct lp_mc {
   int push_mode = 1, pull_mode = 1;   // 0 LDG/STG, 1 TMA
   int64_t chunk_bytes = 16384;
   int window = 3;
+  int wide_loads = 0;
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;   // flag-wait watchdog
   cudaStream_t poll = nullptr;   // private non-blocking stream for host polls
 };
 
@@ -584,10 +601,27 @@ int lp_mc_configure(lp_mc* mc, int direction, int push_mode, int pull_mode, int6
   LP_CHECK(chunk_bytes <= mc->tile_bytes, "lp_mc_configure: chunk larger than a tile");
   if (direction != mc->direction) mc->dirty = true;
   if (window >= 1) mc->window = window < kMaxWindow ? window : kMaxWindow;
+
   mc->direction = direction;
   mc->push_mode = push_mode;
   mc->pull_mode = pull_mode;
   mc->chunk_bytes = chunk_bytes;
+  return 0;
+}
+
+int lp_mc_set_option(lp_mc* mc, const char* name, int64_t value) {
+  LP_CHECK(mc && name, "lp_mc_set_option: null argument");
+  if (!strcmp(name, "wide_loads")) {
+    mc->wide_loads = value != 0;
+  } else if (!strcmp(name, "window")) {
+    LP_CHECK(value >= 1 && value <= kMaxWindow, "lp_mc_set_option: window must be in [1, %d]", kMaxWindow);
+    mc->window = (int)value;
+  } else if (!strcmp(name, "timeout_ms")) {
+    LP_CHECK(value > 0, "lp_mc_set_option: timeout_ms must be positive");
+    mc->timeout_ns = (uint64_t)value * 1000000ull;
+  } else {
+    LP_CHECK(false, "lp_mc_set_option: unknown option '%s'", name);
+  }
   return 0;
 }
 
@@ -613,7 +647,7 @@ int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch, 
   p.recv_blocks = mc->d_recv;
   p.err = mc->d_err;
   p.tile_bytes = mc->tile_bytes;
-  p.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  p.timeout_ns = mc->timeout_ns;
   p.epoch = epoch;
   p.chunk_bytes = (uint32_t)mc->chunk_bytes;
   p.push_ctas = push_ctas;
@@ -622,6 +656,7 @@ int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch, 
   p.pull_mode = mc->pull_mode;
   p.n_exec = n_exec;
   p.window = mc->window;
+  p.wide_loads = mc->wide_loads;
   for (int i = 0; i < n_exec; ++i) {
     int n = exec_nodes[i];
     LP_CHECK(n >= 0 && n < mc->n_nodes, "lp_mc_run: exec node %d out of range", n);

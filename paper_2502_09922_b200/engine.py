@@ -100,6 +100,9 @@ class MulticastEngine:
         0 = LDG/STG vectors, 1 = TMA bulk pipeline; window = ops an LDG CTA may interleave."""
         N.call("lp_mc_configure", self._h, direction, push_mode, pull_mode, chunk_bytes, window)
 
+    def set_option(self, name: str, value: int):
+        N.call("lp_mc_set_option", self._h, name.encode(), int(value))
+
     def reset_signals(self, node: int, stream: int = 0):
         N.call("lp_mc_reset_signals", self._h, node, C.c_void_p(stream or None))
 

@@ -98,8 +98,11 @@ def choose_executor(plan: ScaleOutPlan, tile_bytes: int = E.DEFAULT_TILE):
     with 256 MiB tiles — DMA keeps ~778 GB/s per direction while a relay
     sends and receives, SM-issued NVLink traffic drops to ~673 GB/s —
     everything else (host sources, 1 -> 1) runs in-kernel (2 MiB tiles)."""
-    if not plan.host_source and len(plan.nodes) >= 3:
+    if not plan.host_source and len(plan.nodes) >= 3 and plan.block_count <= 32:
         return "ce", CE_TILE
+    # long schedules (e.g. Llama-3-70B, b = 80: 81 serial ops per relay) lose
+    # more to tile-granular waits on the copy engines than they gain: measured
+    # 295 ms (CE) vs 218-248 ms (kernel) for GPU0 -> 3 peers
     return "kernel", tile_bytes
 
 

@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--window", default="3")
     ap.add_argument("--executor", default="kernel")
     ap.add_argument("--ce-streams", type=int, default=2)
+    ap.add_argument("--wide", default="0")
     a = ap.parse_args()
     rank = 0
     if a.dist:
@@ -54,8 +55,10 @@ def main():
         so = SO.ScaleOut(plan, distributed=a.dist, tile_bytes=tile, device=torch.cuda.current_device(),
                          executor=a.executor, ce_streams=a.ce_streams, direction=a.direction)
         so.load_sources()
-        for chunk, window in [(int(c), int(w)) for c in a.chunk.split(",") for w in a.window.split(",")]:
+        for chunk, window, wide in [(int(c), int(w), int(x)) for c in a.chunk.split(",") for w in a.window.split(",")
+                                    for x in a.wide.split(",")]:
           so.cluster.engine.configure(a.direction, a.push_mode, a.pull_mode, chunk, window)
+          so.cluster.engine.set_option("wide_loads", wide)
           for push in [int(x) for x in a.push.split(",")]:
             for pull in [int(x) for x in a.pull.split(",")]:
                 so.push_ctas, so.pull_ctas = push, pull
@@ -72,7 +75,7 @@ def main():
                         times.append(t.item())
                 best = min(times)
                 med = sorted(times)[len(times) // 2]
-                rec = {"tile": tile, "chunk": chunk, "window": window, "push": push, "pull": pull, "ms_best": round(best, 3),
+                rec = {"tile": tile, "chunk": chunk, "window": window, "wide": wide, "push": push, "pull": pull, "ms_best": round(best, 3),
                        "ms_med": round(med, 3), "agg_GBps": round(R * M / (med * 1e-3) / 1e9, 1),
                        "nvlink_frac": round(M / (900e9 * med * 1e-3), 4),
                        "pcie64_frac": round(M / (64e9 * med * 1e-3), 4)}
