@@ -114,7 +114,9 @@ int lp_mc_configure(lp_mc* mc, int direction, int push_mode, int pull_mode, int6
  * direction 1 (lp_mc_configure): pulls everything it receives; direction 0:
  * pushes everything it sends (waits on its own flags) and pulls host-sourced
  * blocks.  block_events (optional, n_blocks entries, NULL to skip) are
- * recorded after each pulled block's last tile. */
+ * recorded after each pulled block's last tile.  Every stream that may park a
+ * wait needs its own hardware connection (CUDA_DEVICE_MAX_CONNECTIONS >=
+ * streams on the device), else a parked wait stalls unrelated streams. */
 int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
                  void* const* block_events);
 /* tunables: "wide_loads" (0/1: 256 B L2 fetch granule on LDG-role loads),

@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <algorithm>
 #include <string.h>
+#include <stdlib.h>
 #include <vector>
 
 #define LP_MAX_EXEC 32
@@ -46,7 +47,7 @@ struct BlockDev {
   int32_t ntiles;
 };
 struct OpDev {
-  int32_t block, src, dst, wait;
+  int32_t block, src, dst, wait, step, pad;
 };
 struct ExecDesc {
   int32_t node, push_b, push_e, pull_b, pull_e, recv_b, recv_e, pad;
@@ -471,11 +472,11 @@ static int compile(lp_mc* mc) {
     d.node = n;
     d.push_b = (int)ops.size();
     for (const Row& r : rows)
-      if (r.snd == n && !pulled(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1});
+      if (r.snd == n && !pulled(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1, r.step, 0});
     d.push_e = (int)ops.size();
     d.pull_b = (int)ops.size();
     for (const Row& r : rows)
-      if (r.rcv == n && pulled(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1});
+      if (r.rcv == n && pulled(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1, r.step, 0});
     d.pull_e = (int)ops.size();
     // tiles other nodes push into n: waited for before n's kernel completes
     d.recv_b = (int)recv.size();
@@ -713,12 +714,22 @@ int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const
   // direction 0: its copy engine pushes every block it sends (waits are then
   // on its OWN flags, flag writes land in the receiver's memory) and it still
   // pulls host-sourced blocks.  Both run in schedule step order.
+  // one step-ordered sequence of this node's pushes and pulls: a push of a
+  // block this node itself pulls (e.g. from the host) must be enqueued after
+  // that pull, or a single stream would wait on itself
+  std::vector<int> seq;
+  for (int oi = ex.push_b; oi < ex.push_e; ++oi) seq.push_back(oi);
+  for (int oi = ex.pull_b; oi < ex.pull_e; ++oi) seq.push_back(oi);
+  std::stable_sort(seq.begin(), seq.end(),
+                   [&](int a, int b) { return mc->h_ops[a].step < mc->h_ops[b].step; });
   int k = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    const int ob = pass == 0 ? ex.push_b : ex.pull_b;
-    const int oe = pass == 0 ? ex.push_e : ex.pull_e;
-    for (int oi = ob; oi < oe; ++oi, ++k) {
+  const bool dbg = getenv("LP_DEBUG_CE") != nullptr;
+  for (int oi : seq) {
+    {
       const OpDev op = mc->h_ops[oi];
+      if (dbg)
+        fprintf(stderr, "lp_mc_run_ce node %d: op %d step %d %d->%d block %d wait %d stream %d\n", node, oi, op.step,
+                op.src, op.dst, op.block, op.wait, k % n_streams);
       const BlockDev bl = mc->blocks[op.block];
       const NodeDev src = mc->nodes[op.src];
       const NodeDev dst = mc->nodes[op.dst];
@@ -744,9 +755,10 @@ int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const
         r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.ready + op.block), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
         LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: ready write failed (%d)", (int)r);
       }
-      if (block_events && block_events[op.block] && pass == 1)
+      if (block_events && block_events[op.block] && op.dst == node)
         LP_CUDA(cudaEventRecord((cudaEvent_t)block_events[op.block], (cudaStream_t)s));
     }
+    ++k;
   }
   return 0;
 }

@@ -432,7 +432,7 @@ class Cluster:
         self.engine.run(self.exec_nodes, epoch, push_ctas, pull_ctas, stream)
         return epoch
 
-    def ce_streams(self, node: int, count: int = 2) -> list:
+    def ce_streams(self, node: int, count: int = 1) -> list:
         """Per-node torch streams the copy-engine executor enqueues on."""
         import torch
         if not hasattr(self, "_ce"):
@@ -442,7 +442,7 @@ class Cluster:
             self._ce[node] = [torch.cuda.Stream(device=dev) for _ in range(count)]
         return self._ce[node]
 
-    def launch_ce(self, streams_per_node: int = 2, epoch: int | None = None, after=None) -> int:
+    def launch_ce(self, streams_per_node: int = 1, epoch: int | None = None, after=None) -> int:
         """One epoch on copy engines for every exec node; ``after`` = a torch
         event the CE streams wait for first.  Returns the epoch."""
         if epoch is None:

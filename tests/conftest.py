@@ -1,6 +1,12 @@
 import os
 import sys
 
+# The copy-engine executor parks stream-ordered waits (cuStreamWaitValue32) on
+# its streams; emulating many nodes on one GPU needs at least one hardware
+# connection per stream, or a parked wait on a shared connection stalls
+# unrelated streams (the driver default is 8).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -43,7 +43,7 @@ def _worker(rank, world, port, tmp, results):
 def test_two_rank_gloo_plan_partition():
     port = 29000 + os.getpid() % 1000
     with tempfile.TemporaryDirectory() as tmp:
-        mgr = mp.Manager()
+        mgr = mp.get_context("spawn").Manager()
         results = mgr.list()
         mp.spawn(_worker, args=(2, port, tmp, results), nprocs=2, join=True)
         assert len(results) == 6

@@ -54,7 +54,9 @@ def run_case(n, k, b, host, tile, push, pull, oracle_sums, epochs=2, push_mode=1
                 E.N.call("lp_memset", E.C.c_void_p(cl.node(i).image), 0, lay.weights_bytes, None)
             if executor == "ce":
                 import torch
-                cl.launch_ce(2)
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream())   # CE streams must see the memsets above
+                cl.launch_ce(1, after=ev)
                 cl.join_ce(torch.cuda.current_stream())
                 torch.cuda.synchronize()
             else:
@@ -103,7 +105,7 @@ def test_multicast_delivers_source_bytes(n, k, b, host, tile, push, pull, direct
                                              (5, 1, 1, False, 4096)])
 @pytest.mark.parametrize("direction", [0, 1])
 def test_copy_engine_executor_delivers_source_bytes(n, k, b, host, tile, direction, oracle_sums):
-    run_case(n, k, b, host, tile, 0, 1, oracle_sums, direction=direction, executor="ce")
+    run_case(n, k, b, host, tile, 0, 1, oracle_sums, direction=direction, executor="ce", chunk=min(16384, tile))
 
 
 def test_engine_rejects_bad_schedules():
