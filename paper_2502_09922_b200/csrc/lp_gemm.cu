@@ -42,6 +42,8 @@ struct GemmArgs {
   int tokens;         // T (valid tokens)
   int k_blocks;       // ceil(K / BK)
   int kb_per_split;   // k blocks per z-split
+  int atomic;         // EPI_ADD with split-K: red.add; without: plain read-modify-write
+  int tiles_n, tiles_t, splits;   // persistent kernel tile space
 };
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
@@ -228,7 +230,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (t >= args.tokens) break;
           const float a = __uint_as_float(v[j]);
           if (EPI == EPI_ADD_F32) {
-            atomicAdd((float*)args.out + (int64_t)t * args.ldo + n, a);
+            float* o = (float*)args.out + (int64_t)t * args.ldo + n;
+            if (args.atomic) atomicAdd(o, a); else *o += a;
           } else if (EPI == EPI_STORE_F32) {
             ((float*)args.out)[(int64_t)t * args.ldo + n] = a;
           } else {
@@ -245,6 +248,169 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent variant (prefill, T > 64): grid = #SMs, each CTA walks output
+// tiles (weight tile fastest, so neighbouring CTAs share the token tile in
+// L2).  Two TMEM accumulators: the MMA warp fills buffer (i & 1) while the
+// epilogue warps drain buffer ((i - 1) & 1), so the epilogue of one tile
+// overlaps the MMAs of the next; the smem ring runs across tile boundaries.
+
+template <int BT, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmW2,
+                           const __grid_constant__ CUtensorMap tmX, const GemmArgs args) {
+  using C = Cfg<BT, EPI>;
+  static_assert(2 * C::ACC_COLS <= 512, "two accumulators must fit TMEM");
+  constexpr int TCOLS = 2 * C::ACC_COLS <= 32 ? 32 : 2 * C::ACC_COLS <= 64 ? 64 : 2 * C::ACC_COLS <= 128 ? 128
+                        : 2 * C::ACC_COLS <= 256 ? 256 : 512;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[C::STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[C::STAGES];
+  __shared__ __align__(8) uint64_t tfull[2];
+  __shared__ __align__(8) uint64_t tempty[2];
+  __shared__ uint32_t tmem_base_smem;
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int total = args.tiles_n * args.tiles_t * args.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      lp::mbar_init(&full_bar[s], 1);
+      lp::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      lp::mbar_init(&tfull[a], 1);
+      lp::mbar_init(&tempty[a], 4);     // one arrive per epilogue warp
+    }
+    lp::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     lp::smem_u32(&tmem_base_smem)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    if (EPI == EPI_SWIGLU) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW2) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_smem;
+
+  auto tile_coords = [&](int tile, int& n0, int& t0, int& kb0, int& nkb) {
+    const int nt = tile % args.tiles_n;
+    const int rest = tile / args.tiles_n;
+    const int tt = rest % args.tiles_t;
+    const int z = rest / args.tiles_t;
+    n0 = nt * BM;
+    t0 = tt * BT;
+    kb0 = z * args.kb_per_split;
+    nkb = min(args.k_blocks, kb0 + args.kb_per_split) - kb0;
+  };
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int n0, t0, kb0, nkb;
+      tile_coords(tile, n0, t0, kb0, nkb);
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % C::STAGES;
+        lp::mbar_wait(&empty_bar[s], ((it / C::STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        lp::mbar_expect_tx(&full_bar[s], C::STAGE_BYTES);
+        const int kc = (kb0 + i) * BK;
+        tma_load_2d(st, &tmW, &full_bar[s], kc, n0);
+        if (EPI == EPI_SWIGLU) tma_load_2d(st + C::A_BYTES, &tmW2, &full_bar[s], kc, n0);
+        tma_load_2d(st + C::NA * C::A_BYTES, &tmX, &full_bar[s], kc, t0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_bf16_f32<BT>();
+    int it = 0, li = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++li) {
+      int n0, t0, kb0, nkb;
+      tile_coords(tile, n0, t0, kb0, nkb);
+      const int a = li & 1;
+      lp::mbar_wait(&tempty[a], ((li >> 1) & 1) ^ 1);    // epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t acc_base = tmem + a * C::ACC_COLS;
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % C::STAGES;
+        lp::mbar_wait(&full_bar[s], (it / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = lp::smem_u32(smem + s * C::STAGE_BYTES);
+        const uint32_t sb = sa + C::NA * C::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          umma_bf16(acc_base, smem_desc_sw128(sa + kk * 32), smem_desc_sw128(sb + kk * 32), idesc, acc);
+          if (EPI == EPI_SWIGLU)
+            umma_bf16(acc_base + BT, smem_desc_sw128(sa + C::A_BYTES + kk * 32), smem_desc_sw128(sb + kk * 32),
+                      idesc, acc);
+        }
+        umma_commit(&empty_bar[s]);
+      }
+      umma_commit(&tfull[a]);
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue ----------------
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    int li = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++li) {
+      int n0, t0, kb0, nkb;
+      tile_coords(tile, n0, t0, kb0, nkb);
+      const int a = li & 1;
+      lp::mbar_wait(&tfull[a], (li >> 1) & 1);
+      tc_fence_after();
+      const int n = n0 + row;
+      constexpr int CH = BT < 32 ? BT : 32;
+      for (int c = 0; c < BT; c += CH) {
+        uint32_t v[32], u[32];
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * C::ACC_COLS + c;
+        if (CH == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
+        if (EPI == EPI_SWIGLU) {
+          if (CH == 32) tmem_ld32(taddr + BT, u); else tmem_ld16(taddr + BT, u);
+        }
+        tmem_wait_ld();
+        if (n < args.n_rows) {
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = t0 + c + j;
+            if (t >= args.tokens) break;
+            const float x = __uint_as_float(v[j]);
+            if (EPI == EPI_ADD_F32) {
+              float* o = (float*)args.out + (int64_t)t * args.ldo + n;
+              if (args.atomic) atomicAdd(o, x); else *o += x;
+            } else if (EPI == EPI_STORE_F32) {
+              ((float*)args.out)[(int64_t)t * args.ldo + n] = x;
+            } else {
+              const float up = __uint_as_float(u[j]);
+              ((__nv_bfloat16*)args.out)[(int64_t)t * args.ldo + n] =
+                  __float2bfloat16_rn(x / (1.0f + __expf(-x)) * up);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lp::smem_u32(&tempty[a])) : "memory");
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
 }
 
@@ -289,11 +455,14 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
   if (make_map(&mw, W, N, K, BM) != 0) return -1;
   if (make_map(&mw2, EPI == EPI_SWIGLU ? W2 : W, N, K, BM) != 0) return -1;
   if (make_map(&mx, X, T, K, BT) != 0) return -1;
+  const bool persistent = T > 64;
   static uint64_t attr_set = 0;   // per-device bit: the smem opt-in is a per-device function attribute
   int dev = 0;
   LP_CUDA(cudaGetDevice(&dev));
   if (!(attr_set >> dev & 1)) {
     LP_CUDA(cudaFuncSetAttribute(gemm_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    LP_CUDA(cudaFuncSetAttribute(gemm_persistent_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM));
     attr_set |= 1ull << dev;
   }
   GemmArgs a;
@@ -304,8 +473,21 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
   a.k_blocks = (int)((K + BK - 1) / BK);
   const int splits = split_k < 1 ? 1 : (split_k > a.k_blocks ? a.k_blocks : split_k);
   a.kb_per_split = (a.k_blocks + splits - 1) / splits;
-  dim3 grid((unsigned)((N + BM - 1) / BM), (unsigned)((T + BT - 1) / BT), (unsigned)splits);
-  gemm_kernel<BT, EPI><<<grid, THREADS, C::SMEM, s>>>(mw, mw2, mx, a);
+  // fire-and-forget red.add even without split-K: a plain read-modify-write
+  // stalls the epilogue on every load (measured 4x slower at T=4096)
+  a.atomic = 1;
+  a.tiles_n = (int)((N + BM - 1) / BM);
+  a.tiles_t = (int)((T + BT - 1) / BT);
+  a.splits = splits;
+  if (persistent) {
+    static int sms = 0;
+    if (!sms) LP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int total = a.tiles_n * a.tiles_t * a.splits;
+    gemm_persistent_kernel<BT, EPI><<<total < sms ? total : sms, THREADS, C::SMEM, s>>>(mw, mw2, mx, a);
+  } else {
+    dim3 grid((unsigned)a.tiles_n, (unsigned)a.tiles_t, (unsigned)splits);
+    gemm_kernel<BT, EPI><<<grid, THREADS, C::SMEM, s>>>(mw, mw2, mx, a);
+  }
   LP_CUDA(cudaGetLastError());
   return 0;
 }
@@ -316,8 +498,12 @@ int dispatch(const void* W, const void* W2, int64_t N, int64_t K, const void* X,
   if (T <= 16) return launch<16, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
   if (T <= 32) return launch<32, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
   if (T <= 64) return launch<64, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
-  if (EPI == EPI_SWIGLU || T <= 128) return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
-  return launch<256, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  if constexpr (EPI == EPI_SWIGLU) {
+    return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  } else {
+    if (T <= 128) return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+    return launch<256, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  }
 }
 
 }  // namespace
