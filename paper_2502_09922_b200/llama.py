@@ -232,3 +232,70 @@ class DecodeGraph:
             self.graph.replay()
             self.h_out.copy_(self.out, non_blocking=True)
         return self.h_out[:n]
+
+
+class PrefillGraph:
+    """A CUDA graph of one ragged prefill (embed -> all layers -> head on the
+    last row of every request -> argmax) padded to ``tokens`` rows and
+    ``rows`` requests.  Padded token rows sit on the scratch sequence slot at
+    position 0; padded request rows read row 0 and are ignored."""
+
+    def __init__(self, ex: LlamaExecutor, tokens: int, rows: int):
+        import torch
+        self.ex, self.cap, self.rows = ex, tokens, rows
+        dev = ex.torch_device
+        self.d_in = torch.zeros(3 * tokens + rows, dtype=torch.int32, device=dev)
+        self.h_in = torch.zeros(3 * tokens + rows, dtype=torch.int32).pin_memory()
+        self.h_out = torch.zeros(rows, dtype=torch.int32).pin_memory()
+        self.graph = None
+        self.out = None
+
+    def _body(self):
+        c, r = self.cap, self.rows
+        toks, pos, seq = self.d_in[:c], self.d_in[c:2 * c], self.d_in[2 * c:3 * c]
+        last = self.d_in[3 * c:3 * c + r].long()
+        x = self.ex.embed(toks)
+        for l in range(self.ex.layer_lo, self.ex.layer_hi + 1):
+            x = self.ex.layer(l, x, pos, seq)
+        logits = self.ex.head(x.index_select(0, last).contiguous())
+        tok, _ = self.ex.greedy(logits)
+        return tok
+
+    def capture(self):
+        import torch
+        c = self.cap
+        self.d_in[2 * c:3 * c].fill_(self.ex.scratch_seq)
+        with torch.cuda.device(self.ex.device):
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self._body()
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(device=self.ex.device)):
+                self.out = self._body()
+
+    def step(self, tokens, pos, seq, last):
+        """Prefill; returns the next token of each request (pinned host tensor,
+        valid after the device is synchronised)."""
+        import torch
+        c, r = self.cap, self.rows
+        n, m = len(tokens), len(last)
+        if n > c or m > r:
+            raise ValueError("prefill larger than the captured graph")
+        if self.graph is None:
+            self.capture()
+        buf = self.h_in.numpy()
+        buf[:n] = tokens
+        buf[n:c] = 0
+        buf[c:c + n] = pos
+        buf[c + n:2 * c] = 0
+        buf[2 * c:2 * c + n] = seq
+        buf[2 * c + n:3 * c] = self.ex.scratch_seq
+        buf[3 * c:3 * c + m] = last
+        buf[3 * c + m:] = 0
+        with torch.cuda.device(self.ex.device):
+            self.d_in.copy_(self.h_in, non_blocking=True)
+            self.graph.replay()
+            self.h_out.copy_(self.out, non_blocking=True)
+        return self.h_out[:m]

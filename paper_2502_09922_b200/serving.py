@@ -83,6 +83,7 @@ class Unit:
     retired: bool = False
     busy: dict = field(default_factory=dict)   # slot -> Request
     graph: object = None                        # DecodeGraph (local units)
+    prefill: dict = field(default_factory=dict)  # token bucket -> PrefillGraph
 
     @property
     def nodes(self) -> tuple:
@@ -246,6 +247,21 @@ class Server:
             self.log(now, "mode_switch", model=self.cfg.name, nodes=sorted(switched_nodes), mode="local")
         self.switched = True
 
+    PREFILL_BUCKETS = (128, 256, 512, 1024, 2048)
+
+    def _prefill_graph(self, u, n_tokens):
+        """Smallest captured prefill graph that fits (captured on demand)."""
+        if not self.use_graphs:
+            return None
+        for cap in self.PREFILL_BUCKETS:
+            if n_tokens <= cap and cap <= self.max_len * u.slots:
+                if cap not in u.prefill:
+                    from .llama import PrefillGraph
+                    u.prefill[cap] = PrefillGraph(u.stages[0].executor, cap, u.slots)
+                    u.prefill[cap].capture()
+                return u.prefill[cap]
+        return None
+
     def _step_unit(self, u):
         """Enqueue one iteration for unit u; returns [(requests, token tensor)].
 
@@ -265,6 +281,19 @@ class Server:
                 with self.torch.cuda.device(u.stages[0].device):
                     tok = u.graph.step([r.out[-1] for r in dec], [r.kv_len for r in dec], [r.slot for r in dec])
                 out.append((dec, tok))
+            if reqs:
+                pf = self._prefill_graph(u, sum(len(r.prompt) + len(r.out) for r in reqs))
+                if pf is not None:
+                    tokens, pos, seq, last = [], [], [], []
+                    for r in reqs:
+                        ctx = r.prompt + r.out
+                        tokens += ctx
+                        pos += list(range(len(ctx)))
+                        seq += [r.slot] * len(ctx)
+                        last.append(len(tokens) - 1)
+                    with self.torch.cuda.device(u.stages[0].device):
+                        out.append((reqs, pf.step(tokens, pos, seq, last)))
+                    reqs = []
             if not reqs:
                 return out
         tokens, pos, seq, last = [], [], [], []
@@ -311,6 +340,9 @@ class Server:
                 if u.graph is None:
                     u.graph = DecodeGraph(u.stages[0].executor, u.slots)
                     u.graph.capture()
+                for cap in self.PREFILL_BUCKETS:     # prefill graphs too, before the clock
+                    if cap <= self.max_len * u.slots:
+                        self._prefill_graph(u, cap)
         for d in devs:
             torch.cuda.synchronize(d)
         self.t0 = time.perf_counter()

@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int = 16, requests: int = 16,
                 prompt_len: int = 128, out_tokens: int = 32, spacing_s: float = 0.001, pull_ctas: int = 32,
-                local_slots: int = 8, seed: int = 20250815, executor: str = "ce"):
+                local_slots: int = 16, seed: int = 20250815, executor: str = "ce"):
     import numpy as np
     import torch
 
