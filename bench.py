@@ -181,7 +181,9 @@ def main():
     ap.add_argument("--pull-ctas", type=int, default=64)
     ap.add_argument("--no-gpu-source", action="store_true")
     ap.add_argument("--no-serving", action="store_true")
-    ap.add_argument("--requests", type=int, default=16)
+    ap.add_argument("--requests", type=int, default=32)
+    ap.add_argument("--no-burst", action="store_true")
+    ap.add_argument("--burst-compress", type=float, default=60.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -292,6 +294,7 @@ def main():
 
     # --- execute-while-load serving (tokens/s + TTFT during load) ------------
     serving = None
+    burst = None
     if distributed and N >= 3 and not args.no_serving:
         torch.cuda.synchronize()
         # CPU (gloo) barrier: an NCCL barrier would leave a spinning kernel on
@@ -307,6 +310,12 @@ def main():
                                    "(cross-device pipelines); other ranks idle at a barrier")
             except Exception as e:  # noqa: BLE001
                 serving = {"error": f"{type(e).__name__}: {e}"}
+            if not args.no_burst:
+                from burst_bench import run_burst
+                try:
+                    burst = run_burst(N, compress=args.burst_compress)
+                except Exception as e:  # noqa: BLE001
+                    burst = {"error": f"{type(e).__name__}: {e}"}
         dist.barrier(group=cpu_group)
 
     if rank == 0:
@@ -350,6 +359,8 @@ def main():
             line["gpu_source"] = gpu_source
         if serving:
             line["execute_while_load"] = serving
+        if burst:
+            line["bursty_trace"] = burst
         print(json.dumps(line), flush=True)
     if distributed:
         dist.barrier()

@@ -347,6 +347,25 @@ class Cluster:
         cl.per_device = engines
         return cl
 
+    @classmethod
+    def over_buffers(cls, buffers: list, block_offsets, block_lengths, tile_bytes: int = DEFAULT_TILE):
+        """An engine over EXISTING node buffers (no allocation, nothing freed
+        on close): ``buffers[i]`` is the NodeBuffer of op-local node i.  Used
+        by the autoscaling server, which keeps one image + signal area per GPU
+        across repeated scale-outs."""
+        devs = sorted({nb.device for nb in buffers if nb.kind == LP_NODE_GPU})
+        engines = {}
+        for d in devs:
+            N.call("lp_set_device", d)
+            eng = MulticastEngine(len(buffers), block_offsets, block_lengths, tile_bytes)
+            for i, nb in enumerate(buffers):
+                eng.set_node(i, nb.kind, nb.image, nb.signals)
+            engines[d] = eng
+        nodes = [NodeBuffer(i, nb.kind, nb.device, nb.image, nb.signals, []) for i, nb in enumerate(buffers)]
+        cl = cls(engines[devs[0]], nodes, [nb.node for nb in nodes if nb.kind == LP_NODE_GPU])
+        cl.per_device = engines
+        return cl
+
     def node(self, i: int) -> NodeBuffer:
         return self.nodes[i]
 
