@@ -31,6 +31,10 @@ int         lp_version(void);
 const char* lp_last_error(void);
 int lp_device_count(int* n);
 int lp_set_device(int dev);
+/* launch decoder kernels with programmatic dependent launch (this thread);
+ * meant for CUDA-graph capture, where it overlaps each kernel's prologue and
+ * weight prefetch with the previous kernel (env LP_PDL=0 forces it off) */
+int lp_set_pdl(int on);
 int lp_sync_device(int dev);
 /* cudaDeviceEnablePeerAccess(dev -> peer); already-enabled is not an error */
 int lp_enable_peer(int dev, int peer);

@@ -27,6 +27,7 @@ SIGNATURES = {
     "lp_last_error": [],
     "lp_device_count": [_P(C.c_int)],
     "lp_set_device": [C.c_int],
+    "lp_set_pdl": [C.c_int],
     "lp_sync_device": [C.c_int],
     "lp_enable_peer": [C.c_int, C.c_int],
     "lp_malloc": [C.c_int, _i64, _P(_vp)],

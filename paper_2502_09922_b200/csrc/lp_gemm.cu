@@ -168,9 +168,23 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_smem;
 
+  if (threadIdx.x == 0) lp::pdl_trigger();
   if (warp == 0 && lane == 0 && nkb > 0) {
     // ---------------- TMA producer ----------------
-    for (int i = 0; i < nkb; ++i) {
+    // weights do not depend on the previous kernel: the first ring's worth of
+    // weight tiles is requested before waiting for it (PDL), activations after
+    const int pre = nkb < C::STAGES ? nkb : C::STAGES;
+    for (int i = 0; i < pre; ++i) {
+      uint8_t* st = smem + i * C::STAGE_BYTES;
+      lp::mbar_expect_tx(&full_bar[i], C::STAGE_BYTES);
+      const int kc = (kb0 + i) * BK;
+      tma_load_2d(st, &tmW, &full_bar[i], kc, n0);
+      if (EPI == EPI_SWIGLU) tma_load_2d(st + C::A_BYTES, &tmW2, &full_bar[i], kc, n0);
+    }
+    lp::pdl_wait();
+    for (int i = 0; i < pre; ++i)
+      tma_load_2d(smem + i * C::STAGE_BYTES + C::NA * C::A_BYTES, &tmX, &full_bar[i], (kb0 + i) * BK, t0);
+    for (int i = pre; i < nkb; ++i) {
       const int s = i % C::STAGES;
       lp::mbar_wait(&empty_bar[s], ((i / C::STAGES) & 1) ^ 1);
       uint8_t* st = smem + s * C::STAGE_BYTES;
@@ -209,6 +223,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (nkb > 0) {
       lp::mbar_wait(&done_bar, 0);
       tc_fence_after();
+    } else {
+      lp::pdl_wait();
     }
     constexpr int CH = BT < 32 ? BT : 32;
     for (int c = 0; c < BT; c += CH) {
@@ -315,8 +331,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     nkb = min(args.k_blocks, kb0 + args.kb_per_split) - kb0;
   };
 
+  if (threadIdx.x == 0) lp::pdl_trigger();
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
+    lp::pdl_wait();
     int it = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int n0, t0, kb0, nkb;
@@ -483,12 +501,12 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
     static int sms = 0;
     if (!sms) LP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int total = a.tiles_n * a.tiles_t * a.splits;
-    gemm_persistent_kernel<BT, EPI><<<total < sms ? total : sms, THREADS, C::SMEM, s>>>(mw, mw2, mx, a);
+    LP_CUDA(lp::launch(gemm_persistent_kernel<BT, EPI>, dim3(total < sms ? total : sms), dim3(THREADS), C::SMEM, s,
+                       mw, mw2, mx, a));
   } else {
     dim3 grid((unsigned)a.tiles_n, (unsigned)a.tiles_t, (unsigned)splits);
-    gemm_kernel<BT, EPI><<<grid, THREADS, C::SMEM, s>>>(mw, mw2, mx, a);
+    LP_CUDA(lp::launch(gemm_kernel<BT, EPI>, grid, dim3(THREADS), C::SMEM, s, mw, mw2, mx, a));
   }
-  LP_CUDA(cudaGetLastError());
   return 0;
 }
 

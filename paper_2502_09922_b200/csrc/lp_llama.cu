@@ -25,6 +25,8 @@ __device__ __forceinline__ float warp_max(float v) {
 // x[t, :] = float(table[tokens[t], :])
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ table, int64_t d, const int32_t* __restrict__ tokens,
                              float* __restrict__ x) {
+  lp::pdl_wait();
+  lp::pdl_trigger();
   const int t = blockIdx.x;
   const __nv_bfloat16* row = table + (int64_t)tokens[t] * d;
   for (int64_t i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)t * d + i] = __bfloat162float(row[i]);
@@ -33,6 +35,8 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ table, int64_t d,
 // y[t, :] = bf16(x * rsqrt(mean(x^2) + eps) * w)
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w, int64_t d,
                                float eps, __nv_bfloat16* __restrict__ y) {
+  lp::pdl_wait();
+  lp::pdl_trigger();
   const int t = blockIdx.x;
   const float* xr = x + (int64_t)t * d;
   float ss = 0.f;
@@ -59,6 +63,8 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, int H, int KV, int
                                const int32_t* __restrict__ seq, float theta, __nv_bfloat16* __restrict__ q_out,
                                __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
                                int64_t max_len) {
+  lp::pdl_wait();
+  lp::pdl_trigger();
   const int t = blockIdx.x;
   const int p = pos[t];
   const int sq = seq[t];
@@ -102,6 +108,8 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
     int H, int KV, int hd, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
+  lp::pdl_wait();
+  lp::pdl_trigger();
   const int t = blockIdx.x;
   const int kh = blockIdx.y;
   const int G = H / KV;
@@ -166,6 +174,8 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
 // greedy next token: argmax over logits[t, :] (lowest index wins ties)
 __global__ void argmax_kernel(const float* __restrict__ logits, int64_t V, int32_t* __restrict__ out,
                               float* __restrict__ top2 /* optional [T,2]: best, runner-up */) {
+  lp::pdl_wait();
+  lp::pdl_trigger();
   const int t = blockIdx.x;
   const float* row = logits + (int64_t)t * V;
   float best = -INFINITY, second = -INFINITY;
@@ -256,16 +266,15 @@ int lp_handoff(const void* src, void* dst, int64_t bytes, uint32_t* flag, uint32
 
 int lp_embed(const void* table, int64_t d, const int32_t* tokens, int64_t T, float* x, void* stream) {
   LP_CHECK(table && tokens && x && T > 0 && d > 0, "lp_embed: bad arguments");
-  embed_kernel<<<(unsigned)T, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)table, d, tokens, x);
-  LP_CUDA(cudaGetLastError());
+  LP_CUDA(lp::launch(embed_kernel, dim3((unsigned)T), dim3(256), 0, (cudaStream_t)stream,
+                     (const __nv_bfloat16*)table, d, tokens, x));
   return 0;
 }
 
 int lp_rmsnorm(const float* x, const void* w, int64_t T, int64_t d, float eps, void* y, void* stream) {
   LP_CHECK(x && w && y && T > 0 && d > 0, "lp_rmsnorm: bad arguments");
-  rmsnorm_kernel<<<(unsigned)T, 512, 0, (cudaStream_t)stream>>>(x, (const __nv_bfloat16*)w, d, eps,
-                                                                 (__nv_bfloat16*)y);
-  LP_CUDA(cudaGetLastError());
+  LP_CUDA(lp::launch(rmsnorm_kernel, dim3((unsigned)T), dim3(512), 0, (cudaStream_t)stream, x,
+                     (const __nv_bfloat16*)w, d, eps, (__nv_bfloat16*)y));
   return 0;
 }
 
@@ -274,10 +283,9 @@ int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim,
                void* stream) {
   LP_CHECK(qkv && pos && seq && q_out && k_cache && v_cache && T > 0, "lp_rope_kv: bad arguments");
   LP_CHECK(n_kv > 0 && n_heads % n_kv == 0 && head_dim % 2 == 0, "lp_rope_kv: bad head shape");
-  rope_kv_kernel<<<(unsigned)T, 256, 0, (cudaStream_t)stream>>>(qkv, n_heads, n_kv, head_dim, pos, seq, theta,
-                                                                 (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
-                                                                 (__nv_bfloat16*)v_cache, max_len);
-  LP_CUDA(cudaGetLastError());
+  LP_CUDA(lp::launch(rope_kv_kernel, dim3((unsigned)T), dim3(256), 0, (cudaStream_t)stream, qkv, n_heads, n_kv,
+                     head_dim, pos, seq, theta, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
+                     (__nv_bfloat16*)v_cache, max_len));
   return 0;
 }
 
@@ -288,17 +296,15 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
   LP_CHECK(n_kv > 0 && n_heads % n_kv == 0 && n_heads / n_kv <= MAX_G, "lp_attention: GQA group > %d", MAX_G);
   LP_CHECK(head_dim % 32 == 0 && head_dim <= 128, "lp_attention: head_dim must be 32..128, multiple of 32");
   dim3 grid((unsigned)T, (unsigned)n_kv);
-  attention_kernel<<<grid, ATT_WARPS * 32, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)q, (const __nv_bfloat16*)k_cache, (const __nv_bfloat16*)v_cache, pos, seq, n_heads,
-      n_kv, head_dim, max_len, scale, (__nv_bfloat16*)out);
-  LP_CUDA(cudaGetLastError());
+  LP_CUDA(lp::launch(attention_kernel, grid, dim3(ATT_WARPS * 32), 0, (cudaStream_t)stream,
+                     (const __nv_bfloat16*)q, (const __nv_bfloat16*)k_cache, (const __nv_bfloat16*)v_cache, pos, seq,
+                     n_heads, n_kv, head_dim, max_len, scale, (__nv_bfloat16*)out));
   return 0;
 }
 
 int lp_argmax(const float* logits, int64_t T, int64_t V, int32_t* out, float* top2, void* stream) {
   LP_CHECK(logits && out && T > 0 && V > 0, "lp_argmax: bad arguments");
-  argmax_kernel<<<(unsigned)T, 1024, 0, (cudaStream_t)stream>>>(logits, V, out, top2);
-  LP_CUDA(cudaGetLastError());
+  LP_CUDA(lp::launch(argmax_kernel, dim3((unsigned)T), dim3(1024), 0, (cudaStream_t)stream, logits, V, out, top2));
   return 0;
 }
 

@@ -3,9 +3,19 @@
 #include "lp_common.cuh"
 #include "../../include/lambdapipe.h"
 #include <string.h>
+#include <stdlib.h>
 
 namespace lp {
 static thread_local char g_err[1024] = "";
+static thread_local int g_pdl = 0;
+bool pdl_enabled() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("LP_PDL");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1 && g_pdl == 1;
+}
 void set_error(const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -17,6 +27,10 @@ void set_error(const char* fmt, ...) {
 extern "C" {
 
 int lp_version(void) { return 100; }
+int lp_set_pdl(int on) {
+  lp::g_pdl = on ? 1 : 0;
+  return 0;
+}
 const char* lp_last_error(void) { return lp::g_err; }
 
 int lp_device_count(int* n) {

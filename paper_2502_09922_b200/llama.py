@@ -212,8 +212,12 @@ class DecodeGraph:
             self.graph = torch.cuda.CUDAGraph()
             # explicit per-device capture stream: torch.cuda.graph's default side
             # stream is created once, on whichever device captured first
-            with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(device=self.ex.device)):
-                self.out = self._body()
+            N.lib().lp_set_pdl(1)
+            try:
+                with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(device=self.ex.device)):
+                    self.out = self._body()
+            finally:
+                N.lib().lp_set_pdl(0)
 
     def step(self, tokens, pos, seq):
         """Decode one token for each live row; returns the int32 device tensor."""
@@ -272,8 +276,12 @@ class PrefillGraph:
                 self._body()
             torch.cuda.current_stream().wait_stream(s)
             self.graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(device=self.ex.device)):
-                self.out = self._body()
+            N.lib().lp_set_pdl(1)
+            try:
+                with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(device=self.ex.device)):
+                    self.out = self._body()
+            finally:
+                N.lib().lp_set_pdl(0)
 
     def step(self, tokens, pos, seq, last):
         """Prefill; returns the next token of each request (pinned host tensor,
