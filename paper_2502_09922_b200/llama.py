@@ -307,3 +307,134 @@ class PrefillGraph:
             self.graph.replay()
             self.h_out.copy_(self.out, non_blocking=True)
         return self.h_out[:m]
+
+
+class SegmentGraph:
+    """One captured piece of a pipeline stage, with static device I/O:
+
+    * ``embed``: tokens -> x (vocab stage only),
+    * layers [ex.layer_lo, ex.layer_hi] on x,
+    * ``head``: rows ``last`` of x -> final norm -> LM head -> argmax,
+
+    padded to ``cap`` token rows and ``rows`` requests (padding on the
+    executor's scratch sequence slot).  ``x_in`` / ``x_out`` are the fixed
+    hand-off buffers the previous / next stage reads and writes."""
+
+    def __init__(self, ex: LlamaExecutor, cap: int, rows: int, embed: bool, layers: bool, head: bool):
+        import torch
+        self.ex, self.cap, self.rows = ex, cap, rows
+        self.embed_, self.layers_, self.head_ = embed, layers, head
+        dev = ex.torch_device
+        d = ex.cfg.d_model
+        self.d_in = torch.zeros(3 * cap + rows, dtype=torch.int32, device=dev)
+        self.h_in = torch.zeros(3 * cap + rows, dtype=torch.int32).pin_memory()
+        self.x_in = torch.zeros((cap, d), dtype=torch.float32, device=dev)
+        self.x_out = torch.zeros((cap, d), dtype=torch.float32, device=dev)
+        self.h_out = torch.zeros(rows, dtype=torch.int32).pin_memory()
+        self.graph = None
+        self.tok = None
+
+    def _body(self):
+        c, r = self.cap, self.rows
+        toks, pos, seq = self.d_in[:c], self.d_in[c:2 * c], self.d_in[2 * c:3 * c]
+        x = self.ex.embed(toks) if self.embed_ else self.x_in.clone()
+        if self.layers_:
+            for l in range(self.ex.layer_lo, self.ex.layer_hi + 1):
+                x = self.ex.layer(l, x, pos, seq)
+        if self.head_:
+            last = self.d_in[3 * c:3 * c + r].long()
+            logits = self.ex.head(x.index_select(0, last).contiguous())
+            tok, _ = self.ex.greedy(logits)
+            return tok
+        self.x_out.copy_(x)
+        return None
+
+    def capture(self):
+        import torch
+        c = self.cap
+        self.d_in[2 * c:3 * c].fill_(self.ex.scratch_seq)
+        with torch.cuda.device(self.ex.device):
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self._body()
+            torch.cuda.current_stream().wait_stream(s)
+            self.graph = torch.cuda.CUDAGraph()
+            N.lib().lp_set_pdl(1)
+            try:
+                with torch.cuda.graph(self.graph, stream=torch.cuda.Stream(device=self.ex.device)):
+                    self.tok = self._body()
+            finally:
+                N.lib().lp_set_pdl(0)
+
+    def stage_inputs(self, tokens, pos, seq, last):
+        c = self.cap
+        n, m = len(tokens), len(last)
+        buf = self.h_in.numpy()
+        buf[:n] = tokens
+        buf[n:c] = 0
+        buf[c:c + n] = pos
+        buf[c + n:2 * c] = 0
+        buf[2 * c:2 * c + n] = seq
+        buf[2 * c + n:3 * c] = self.ex.scratch_seq
+        buf[3 * c:3 * c + m] = last
+        buf[3 * c + m:] = 0
+        self.d_in.copy_(self.h_in, non_blocking=True)
+
+
+class PipelineGraph:
+    """Graph-replayed forward of an execution pipeline: one SegmentGraph per
+    stage (the vocab stage embeds; a separate head segment on the vocab
+    device closes the ring) with NVLink hand-offs (``lp_handoff``) between
+    devices, ordered by CUDA events — no host round trip inside a step."""
+
+    def __init__(self, stage_execs: list, vocab_exec: LlamaExecutor, cap: int, rows: int):
+        self.cap, self.rows = cap, rows
+        self.segs = []
+        for i, ex in enumerate(stage_execs):
+            self.segs.append(SegmentGraph(ex, cap, rows, embed=(i == 0), layers=ex.layer_lo <= ex.layer_hi,
+                                          head=False))
+        self.head = SegmentGraph(vocab_exec, cap, rows, embed=False, layers=False, head=True)
+
+    def capture(self):
+        for g in self.segs + [self.head]:
+            g.capture()
+
+    def _handoff(self, src, dst):
+        import torch
+        sdev, ddev = src.device.index, dst.device.index
+        if sdev == ddev:
+            with torch.cuda.device(sdev):
+                dst.copy_(src)
+            return
+        with torch.cuda.device(sdev):
+            N.check(N.lib().lp_handoff(C.c_void_p(src.data_ptr()), C.c_void_p(dst.data_ptr()),
+                                       src.numel() * src.element_size(), None, 0, None,
+                                       C.c_void_p(torch.cuda.current_stream(sdev).cuda_stream)), "lp_handoff")
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(sdev))
+        torch.cuda.current_stream(ddev).wait_event(ev)
+
+    def step(self, tokens, pos, seq, last):
+        """One ragged batch through the ring; returns the next token per
+        request (pinned host tensor, valid once the vocab device is synced)."""
+        import torch
+        if len(tokens) > self.cap or len(last) > self.rows:
+            raise ValueError("batch larger than the captured pipeline graph")
+        if self.head.graph is None:
+            self.capture()
+        prev = None
+        for g in self.segs:
+            with torch.cuda.device(g.ex.device):
+                g.stage_inputs(tokens, pos, seq, last)
+                if prev is not None:
+                    self._handoff(prev, g.x_in)
+                g.graph.replay()
+            prev = g.x_out
+        h = self.head
+        with torch.cuda.device(h.ex.device):
+            h.stage_inputs(tokens, pos, seq, last)
+            self._handoff(prev, h.x_in)
+            h.graph.replay()
+            h.h_out.copy_(h.tok, non_blocking=True)
+        return h.h_out[:len(last)]

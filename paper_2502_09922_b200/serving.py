@@ -262,6 +262,23 @@ class Server:
                 return u.prefill[cap]
         return None
 
+    def _pipeline_graph(self, u, n_tokens):
+        """Captured ring for a pipeline unit: decode width = slots, prefill
+        buckets like local replicas (captured on demand, or before the clock)."""
+        if not self.use_graphs:
+            return None
+        from .llama import PipelineGraph
+        vocab = next(st for st in u.stages if st.vocab).executor
+        execs = [st.executor for st in u.stages]
+        caps = [u.slots] + [c for c in self.PREFILL_BUCKETS if c <= self.max_len * u.slots]
+        for cap in caps:
+            if n_tokens <= cap:
+                if cap not in u.prefill:
+                    u.prefill[cap] = PipelineGraph(execs, vocab, cap, u.slots)
+                    u.prefill[cap].capture()
+                return u.prefill[cap]
+        return None
+
     def _step_unit(self, u):
         """Enqueue one iteration for unit u; returns [(requests, token tensor)].
 
@@ -308,6 +325,10 @@ class Server:
                 pos.append(r.kv_len)
                 seq.append(r.slot)
             last.append(len(tokens) - 1)
+        pg = self._pipeline_graph(u, len(tokens)) if u.kind == "pipeline" else None
+        if pg is not None:
+            out.append((reqs, pg.step(tokens, pos, seq, last)))
+            return out
         tok = self._forward(u, tokens, pos, seq, last)
         out.append((reqs, tok))
         return out
@@ -343,6 +364,11 @@ class Server:
                 for cap in self.PREFILL_BUCKETS:     # prefill graphs too, before the clock
                     if cap <= self.max_len * u.slots:
                         self._prefill_graph(u, cap)
+            for u in self.units.values():
+                if u.kind == "pipeline":
+                    for cap in [u.slots] + list(self.PREFILL_BUCKETS):
+                        if cap <= self.max_len * u.slots:
+                            self._pipeline_graph(u, cap)
         for d in devs:
             torch.cuda.synchronize(d)
         self.t0 = time.perf_counter()
