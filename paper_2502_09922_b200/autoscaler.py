@@ -290,7 +290,9 @@ class AutoscaleServer(Server):
                 time.sleep(0.0005)
                 continue
             for d in {st.device for u, _ in work for st in u.stages}:
-                torch.cuda.synchronize(d)
+                # the compute stream only: a device-wide sync would also wait for the
+                # multicast still landing blocks on its own stream
+                torch.cuda.current_stream(d).synchronize()
             now = time.perf_counter() - self.t0
             for u, (reqs, tok) in work:
                 for r, t in zip(reqs, tok.cpu().tolist()):

@@ -124,6 +124,7 @@ class Server:
         self.torch = torch
         self.receivers = [n for n in plan.receivers if cluster.node(n).kind == 0]
         self.block_complete_s = {}      # node -> time it held every block
+        self.activation_s = {}          # pipeline unit -> time its stages' blocks had all landed
         # pipeline units from the plan (one per ExecutionPipeline)
         for ep in plan.pipelines:
             stages = []
@@ -404,6 +405,7 @@ class Server:
                         if all(all(done[st.node][b] for b in range(st.block_lo, st.block_hi + 1))
                                for st in u.stages):
                             u.active = True
+                            self.activation_s[u.uid] = now
                 all_done = all(all(done[n]) for n in self.receivers)
                 if all_done and tokens_emitted >= self.switch_hold_tokens:
                     self._mode_switch(now)
@@ -421,7 +423,9 @@ class Server:
                 continue
             t_sync = time.perf_counter()
             for d in {u.stages[0].device for u, _ in work} | {st.device for u, _ in work for st in u.stages}:
-                torch.cuda.synchronize(d)
+                # the compute stream only: a device-wide sync would also wait for the
+                # multicast still landing blocks on its own stream
+                torch.cuda.current_stream(d).synchronize()
             t_done = time.perf_counter()
             self.profile.append((t_enq - self.t0, t_sync - t_enq, t_done - t_sync,
                                  sum(len(w[0]) for _, w in work), sum(1 for _, w in work)))

@@ -12,6 +12,8 @@ import json
 import os
 import sys
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")   # see paper_2502_09922_b200/__init__.py
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
@@ -74,6 +76,7 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
             "workload": f"{model} bf16, GPU sources {plan.sources}, receivers {plan.receivers}, b={blocks}, k={k}; "
                         f"{requests} requests x (prompt {prompt_len}, out {out_tokens}), {spacing_s * 1e3:.0f} ms apart at t=0",
             "pipelines": [[(st.node, st.block_lo, st.block_hi) for st in ep.stages] for ep in plan.pipelines],
+            "pipeline_activation_s": sorted(srv2.activation_s.values()),
             "first_token_s": rep.first_token_s, "first_receiver_full_model_s": first_full,
             "all_receivers_full_s": all_full, "mode_switch_s": t_switch,
             "tokens_before_switch": pipe_tokens,
@@ -97,5 +100,8 @@ if __name__ == "__main__":
     ap.add_argument("--blocks", type=int, default=16)
     ap.add_argument("--requests", type=int, default=16)
     ap.add_argument("--out-tokens", type=int, default=32)
+    ap.add_argument("--executor", default="ce")
+    ap.add_argument("--pull-ctas", type=int, default=32)
     a = ap.parse_args()
-    print(json.dumps(run_serving(a.gpus, a.model, a.k, a.blocks, a.requests, out_tokens=a.out_tokens)))
+    print(json.dumps(run_serving(a.gpus, a.model, a.k, a.blocks, a.requests, out_tokens=a.out_tokens,
+                                 executor=a.executor, pull_ctas=a.pull_ctas)))
