@@ -190,6 +190,7 @@ class DecodeGraph:
         # pinned staging: one H2D copy of [tokens | pos | seq], one D2H of the result
         self.h_in = torch.zeros(3 * batch, dtype=torch.int32).pin_memory()
         self.d_in = torch.zeros(3 * batch, dtype=torch.int32, device=dev)
+        self.d_in[2 * batch:] = ex.scratch_seq   # warm-up/capture rows must only touch the scratch slot
         self.h_out = torch.zeros(batch, dtype=torch.int32).pin_memory()
 
     def _body(self):

@@ -456,3 +456,48 @@ class Server:
             torch.cuda.synchronize(d)
         self.requests = live
         return self.events
+
+
+def generate(executor, prompts: list, max_new_tokens: int, use_graph: bool = True) -> list:
+    """Greedy generation on one local replica — the reference has no
+    ``generate()``; its per-request token loop (simengine.py:370-378,
+    690-712) is the analogue.  ``executor`` is a full-model
+    ``llama.LlamaExecutor``; ``prompts`` lists token-id lists (at most the
+    executor's sequence slots).  Prefill is one ragged batch, decode steps
+    replay a captured graph.  Returns the generated token lists."""
+    import torch
+    from .llama import DecodeGraph
+    n = len(prompts)
+    if n > executor.scratch_seq:
+        raise ValueError("more prompts than the executor's sequence slots")
+    dev = executor.torch_device
+    toks, pos, seq, last = [], [], [], []
+    for i, p in enumerate(prompts):
+        toks += list(p)
+        pos += list(range(len(p)))
+        seq += [i] * len(p)
+        last.append(len(toks) - 1)
+    with torch.cuda.device(executor.device):
+        t = torch.as_tensor(toks, dtype=torch.int32, device=dev)
+        x, _ = executor.forward(tokens=t, pos=torch.as_tensor(pos, dtype=torch.int32, device=dev),
+                                seq=torch.as_tensor(seq, dtype=torch.int32, device=dev), want_logits=False)
+        logits = executor.head(x[torch.as_tensor(last, device=dev)].contiguous())
+        nxt, _ = executor.greedy(logits)
+        out = [[v] for v in nxt.cpu().tolist()]
+        kv = [len(p) for p in prompts]
+        graph = DecodeGraph(executor, n) if use_graph else None
+        for _ in range(max_new_tokens - 1):
+            cur = [o[-1] for o in out]
+            if graph is not None:
+                res = graph.step(cur, kv, list(range(n)))
+                torch.cuda.current_stream().synchronize()
+                vals = res.tolist()
+            else:
+                _, lg = executor.forward(tokens=torch.as_tensor(cur, dtype=torch.int32, device=dev),
+                                         pos=torch.as_tensor(kv, dtype=torch.int32, device=dev),
+                                         seq=torch.arange(n, dtype=torch.int32, device=dev))
+                vals = executor.greedy(lg)[0].cpu().tolist()
+            for o, v in zip(out, vals):
+                o.append(int(v))
+            kv = [k + 1 for k in kv]
+    return out

@@ -125,3 +125,21 @@ def test_stage_split_equals_local(tiny):
     x, _ = s1.forward(x=x.clone(), pos=pos, seq=seq, want_logits=False)
     lg = s0.head(x)
     assert (lg - ref).abs().max().item() < 1e-2
+
+
+def test_generate_api_matches_oracle(tiny):
+    """serving.generate(): batched prefill + graph decode == oracle greedy."""
+    from oracle import llama as OL
+    from paper_2502_09922_b200.llama import LlamaExecutor
+    from paper_2502_09922_b200.serving import generate
+    cfg, lay, W, ptr = tiny
+    rng = np.random.default_rng(11)
+    prompts = [rng.integers(0, cfg.vocab, 9 + 3 * i).tolist() for i in range(3)]
+    ex = LlamaExecutor(lay, ptr, 0, max_seqs=4, max_len=48)
+    outs = generate(ex, prompts, 8)
+    for p, got in zip(prompts, outs):
+        ref, margins = OL.greedy(cfg, W, p, 8)
+        for i, (a, b) in enumerate(zip(got, ref)):
+            if margins[i] < 2 * LOGIT_TOL:
+                break
+            assert a == b, (got, ref, margins)
