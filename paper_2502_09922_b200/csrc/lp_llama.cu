@@ -65,45 +65,41 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, int H, int KV, int
                                int64_t max_len) {
   lp::pdl_wait();
   lp::pdl_trigger();
+  // grid (T, H + 2*KV): one CTA per (token, head); v heads are copied
   const int t = blockIdx.x;
+  const int head = blockIdx.y;
   const int p = pos[t];
   const int sq = seq[t];
   const int half = hd / 2;
-  const float* row = qkv + (int64_t)t * (H + 2 * KV) * hd;
-  for (int idx = threadIdx.x; idx < (H + KV) * half; idx += blockDim.x) {
-    const int head = idx / half;
-    const int j = idx % half;
-    const float inv = powf(theta, -2.0f * (float)j / (float)hd);
+  const float* src = qkv + ((int64_t)t * (H + 2 * KV) + head) * hd;
+  if (head >= H + KV) {
+    const int kh = head - H - KV;
+    __nv_bfloat16* dst = v_cache + (((int64_t)sq * KV + kh) * max_len + p) * hd;
+    for (int j = threadIdx.x; j < hd; j += blockDim.x) dst[j] = __float2bfloat16_rn(src[j]);
+    return;
+  }
+  __nv_bfloat16* dst = head < H ? q_out + ((int64_t)t * H + head) * hd
+                                : k_cache + (((int64_t)sq * KV + (head - H)) * max_len + p) * hd;
+  const float l2t = log2f(theta);
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    const float inv = exp2f(-2.0f * (float)j / (float)hd * l2t);
     float sn, cs;
     sincosf((float)p * inv, &sn, &cs);
-    const float* src = row + head * hd;
     const float a = src[j], b = src[j + half];
-    const float ra = a * cs - b * sn;
-    const float rb = b * cs + a * sn;
-    if (head < H) {
-      __nv_bfloat16* dst = q_out + ((int64_t)t * H + head) * hd;
-      dst[j] = __float2bfloat16_rn(ra);
-      dst[j + half] = __float2bfloat16_rn(rb);
-    } else {
-      const int kh = head - H;
-      __nv_bfloat16* dst = k_cache + (((int64_t)sq * KV + kh) * max_len + p) * hd;
-      dst[j] = __float2bfloat16_rn(ra);
-      dst[j + half] = __float2bfloat16_rn(rb);
-    }
-  }
-  for (int idx = threadIdx.x; idx < KV * hd; idx += blockDim.x) {
-    const int kh = idx / hd;
-    const int j = idx % hd;
-    v_cache[(((int64_t)sq * KV + kh) * max_len + p) * hd + j] =
-        __float2bfloat16_rn(row[(H + KV) * hd + kh * hd + j]);
+    dst[j] = __float2bfloat16_rn(a * cs - b * sn);
+    dst[j + half] = __float2bfloat16_rn(b * cs + a * sn);
   }
 }
 
 // One CTA per (token, kv head); its G = H/KV query heads attend over keys
-// 0..pos of the token's sequence.  Warps split the keys (online softmax per
-// warp, merged through smem).  head_dim <= 128 (lanes hold hd/32 dims).
-constexpr int ATT_WARPS = 8;
+// 0..pos of the token's sequence.  Lane-per-key: each warp takes chunks of 32
+// keys, every lane computes its key's G dot products from 16-byte K loads
+// against q in smem (no per-key shuffles), one max/sum reduction per chunk,
+// then P.V with the chunk's probabilities broadcast lane by lane while each
+// lane accumulates its hd/32 output dims.  Warps merge through smem.
+constexpr int ATT_WARPS = 4;
 constexpr int MAX_G = 8;
+constexpr int MAX_HD = 128;
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
@@ -115,39 +111,87 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
   const int G = H / KV;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = pos[t] + 1;
-  const int per = hd / 32;  // dims per lane (<= 4)
+  const int per = hd / 32;  // output dims per lane (<= 4)
   const __nv_bfloat16* kb = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * hd;
   const __nv_bfloat16* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * hd;
-  float qr[MAX_G][4], acc[MAX_G][4], m[MAX_G], l[MAX_G];
-  for (int g = 0; g < G; ++g) {
-    const __nv_bfloat16* qh = q + ((int64_t)t * H + kh * G + g) * hd;
-    for (int i = 0; i < per; ++i) {
-      qr[g][i] = __bfloat162float(qh[lane * per + i]) * scale;
-      acc[g][i] = 0.f;
-    }
+  __shared__ float sq[MAX_G][MAX_HD];
+  for (int i = threadIdx.x; i < G * hd; i += blockDim.x) {
+    const int g = i / hd, dd = i % hd;
+    sq[g][dd] = __bfloat162float(q[((int64_t)t * H + kh * G + g) * hd + dd]) * scale;
+  }
+  __syncthreads();
+  float m[MAX_G], l[MAX_G], acc[MAX_G][4];
+#pragma unroll
+  for (int g = 0; g < MAX_G; ++g) {
     m[g] = -INFINITY;
     l[g] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[g][i] = 0.f;
   }
-  for (int j = warp; j < L; j += ATT_WARPS) {
-    float kv[4], vv[4];
-    for (int i = 0; i < per; ++i) {
-      kv[i] = __bfloat162float(kb[(int64_t)j * hd + lane * per + i]);
-      vv[i] = __bfloat162float(vb[(int64_t)j * hd + lane * per + i]);
+  for (int c0 = warp * 32; c0 < L; c0 += ATT_WARPS * 32) {
+    const int j = c0 + lane;
+    const bool live = j < L;
+    float s[MAX_G];
+#pragma unroll
+    for (int g = 0; g < MAX_G; ++g) s[g] = 0.f;
+    if (live) {
+      const int4* kr = reinterpret_cast<const int4*>(kb + (int64_t)j * hd);
+      for (int v8 = 0; v8 < hd / 8; ++v8) {
+        const int4 raw = kr[v8];
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+        float kf[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          kf[2 * e] = f.x;
+          kf[2 * e + 1] = f.y;
+        }
+#pragma unroll
+        for (int g = 0; g < MAX_G; ++g) {
+          if (g < G) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s[g] += sq[g][v8 * 8 + e] * kf[e];
+          }
+        }
+      }
     }
-    for (int g = 0; g < G; ++g) {
-      float s = 0.f;
-      for (int i = 0; i < per; ++i) s += qr[g][i] * kv[i];
-      s = warp_sum(s);
-      const float mn = fmaxf(m[g], s);
+    float p[MAX_G];
+#pragma unroll
+    for (int g = 0; g < MAX_G; ++g) {
+      if (g >= G) break;
+      const float cm = warp_max(live ? s[g] : -INFINITY);
+      const float mn = fmaxf(m[g], cm);
       const float corr = __expf(m[g] - mn);
-      const float pexp = __expf(s - mn);
-      l[g] = l[g] * corr + pexp;
-      for (int i = 0; i < per; ++i) acc[g][i] = acc[g][i] * corr + pexp * vv[i];
+      p[g] = live ? __expf(s[g] - mn) : 0.f;
+      l[g] = l[g] * corr + warp_sum(p[g]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[g][i] *= corr;
       m[g] = mn;
+    }
+    const int nk = min(32, L - c0);
+    for (int jj = 0; jj < nk; ++jj) {
+      const __nv_bfloat16* vr = vb + (int64_t)(c0 + jj) * hd + lane * per;
+      float vf[4];
+      if (per == 4) {
+        const uint2 raw = *reinterpret_cast<const uint2*>(vr);
+        const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+        const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+        vf[0] = f0.x; vf[1] = f0.y; vf[2] = f1.x; vf[3] = f1.y;
+      } else {
+        for (int i = 0; i < per; ++i) vf[i] = __bfloat162float(vr[i]);
+      }
+#pragma unroll
+      for (int g = 0; g < MAX_G; ++g) {
+        if (g >= G) break;
+        const float pj = __shfl_sync(0xffffffffu, p[g], jj);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < per) acc[g][i] += pj * vf[i];
+      }
     }
   }
   __shared__ float sm_m[ATT_WARPS][MAX_G], sm_l[ATT_WARPS][MAX_G];
-  __shared__ float sm_acc[ATT_WARPS][MAX_G][128];
+  __shared__ float sm_acc[ATT_WARPS][MAX_G][MAX_HD];
   for (int g = 0; g < G; ++g) {
     if (lane == 0) {
       sm_m[warp][g] = m[g];
@@ -283,7 +327,7 @@ int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim,
                void* stream) {
   LP_CHECK(qkv && pos && seq && q_out && k_cache && v_cache && T > 0, "lp_rope_kv: bad arguments");
   LP_CHECK(n_kv > 0 && n_heads % n_kv == 0 && head_dim % 2 == 0, "lp_rope_kv: bad head shape");
-  LP_CUDA(lp::launch(rope_kv_kernel, dim3((unsigned)T), dim3(256), 0, (cudaStream_t)stream, qkv, n_heads, n_kv,
+  LP_CUDA(lp::launch(rope_kv_kernel, dim3((unsigned)T, (unsigned)(n_heads + 2 * n_kv)), dim3(64), 0, (cudaStream_t)stream, qkv, n_heads, n_kv,
                      head_dim, pos, seq, theta, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
                      (__nv_bfloat16*)v_cache, max_len));
   return 0;
