@@ -23,6 +23,7 @@
 #include "lp_common.cuh"
 #include "../../include/lambdapipe.h"
 #include <cuda.h>
+#include <stdlib.h>
 #include <mutex>
 #include <unordered_map>
 
@@ -473,7 +474,15 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
   if (make_map(&mw, W, N, K, BM) != 0) return -1;
   if (make_map(&mw2, EPI == EPI_SWIGLU ? W2 : W, N, K, BM) != 0) return -1;
   if (make_map(&mx, X, T, K, BT) != 0) return -1;
-  const bool persistent = T > 64;
+  // persistent (grid-stride over (tile, split) work items) for prefill; for
+  // decode when LP_GEMM_STREAMK=1 (experiment: split-K items balanced over
+  // 2 CTAs per SM instead of one wave of fixed tiles)
+  static int streamk = -1;
+  if (streamk < 0) {
+    const char* e = getenv("LP_GEMM_STREAMK");
+    streamk = (e && e[0] == '1') ? 1 : 0;
+  }
+  const bool persistent = T > 64 || streamk;
   static uint64_t attr_set = 0;   // per-device bit: the smem opt-in is a per-device function attribute
   int dev = 0;
   LP_CUDA(cudaGetDevice(&dev));
@@ -501,8 +510,9 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
     static int sms = 0;
     if (!sms) LP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int total = a.tiles_n * a.tiles_t * a.splits;
-    LP_CUDA(lp::launch(gemm_persistent_kernel<BT, EPI>, dim3(total < sms ? total : sms), dim3(THREADS), C::SMEM, s,
-                       mw, mw2, mx, a));
+    const int slots = (T > 64 ? 1 : 2) * sms;      // small decode rings fit two CTAs per SM
+    LP_CUDA(lp::launch(gemm_persistent_kernel<BT, EPI>, dim3(total < slots ? total : slots), dim3(THREADS), C::SMEM,
+                       s, mw, mw2, mx, a));
   } else {
     dim3 grid((unsigned)a.tiles_n, (unsigned)a.tiles_t, (unsigned)splits);
     LP_CUDA(lp::launch(gemm_kernel<BT, EPI>, grid, dim3(THREADS), C::SMEM, s, mw, mw2, mx, a));
