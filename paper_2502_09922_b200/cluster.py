@@ -14,7 +14,7 @@ import math
 from dataclasses import dataclass
 
 from .errors import InvalidArgumentError
-from .multicast import BlockPlan, MulticastSchedule
+from .multicast import BlockPlan, MulticastSchedule, SubGroup, Transfer
 
 STRATEGIES = ("lambda_scale", "binary_tree", "broadcast_groups", "ssd_only", "ideal")
 
@@ -84,3 +84,42 @@ def transfer_step_time(schedule: MulticastSchedule, plan: BlockPlan, cluster: Cl
     """Modelled seconds per lockstep step: ovh + mean block × degree / fabric BW."""
     return cluster.step_fixed_overhead_s + \
         plan.mean_block_bytes() * schedule.max_send_degree / cluster.nic_Bps
+
+
+def baseline_schedule(strategy: str, nodes: list, plan: BlockPlan, cluster: ClusterSpec) -> MulticastSchedule:
+    """Comparator schedules of the reference (simengine.py:106-151), executed
+    for real by the multicast engine (tools/compare_strategies.py):
+
+    * ``binary_tree`` — static breadth-first tree (FaaSNet-style), block j
+      crosses into node i at step j + depth(i) - 1, parents feed both children
+      in the same step (``max_send_degree = 2``);
+    * ``broadcast_groups`` — per-block recursive-doubling broadcast behind a
+      one-time group-formation delay (NCCL-style), no step bound;
+    * ``ssd_only`` / ``ideal`` — no network plan, one group per node.
+    """
+    order = tuple(bl.block_id for bl in plan.blocks)
+    nblk = len(order)
+    n = len(nodes)
+    if strategy == "binary_tree":
+        depth = [0] * n
+        for i in range(1, n):
+            depth[i] = depth[(i - 1) // 2] + 1
+        horizon = nblk + max(depth) - 1 if n > 1 else 0
+        steps = []
+        for st in range(horizon):
+            steps.append([Transfer(st, nodes[(i - 1) // 2], nodes[i], order[st - depth[i] + 1])
+                          for i in range(1, n) if 0 <= st - depth[i] + 1 < nblk])
+        return MulticastSchedule((SubGroup(0, tuple(nodes), order),), steps, max_send_degree=2, label=strategy)
+    if strategy == "broadcast_groups":
+        rounds = max(1, math.ceil(math.log2(n))) if n > 1 else 0
+        steps = []
+        for blk in order:
+            for d in range(rounds):
+                idx = len(steps)
+                steps.append([Transfer(idx, nodes[p], nodes[p + (1 << d)], blk)
+                              for p in range(1 << d) if p + (1 << d) < n])
+        return MulticastSchedule((SubGroup(0, tuple(nodes), order),), steps, enforce_step_bound=False,
+                                 initial_delay_s=cluster.baseline_group_init_s, label=strategy)
+    if strategy in ("ssd_only", "ideal"):
+        return MulticastSchedule(tuple(SubGroup(i, (x,), order) for i, x in enumerate(nodes)), [], label=strategy)
+    raise InvalidArgumentError(f"unknown strategy {strategy!r}")

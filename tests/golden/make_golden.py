@@ -283,6 +283,15 @@ def make_misc():
                     d = S.autoscale(pol, q, a, idle)
                     m["autoscale"].append([pol.threshold_hi, pol.capacity_per_replica, pol.min_replicas,
                                            q, a, idle, d.scale_out, d.scale_in])
+    m["baseline_schedule"] = []
+    for strat in ("binary_tree", "broadcast_groups", "ssd_only", "ideal"):
+        for n, b in ((1, 4), (2, 4), (3, 5), (8, 16), (9, 7), (5, 1)):
+            plan = partition_blocks(ModelSpec("m", 26 * GB, 80), b)
+            sc = S.baseline_schedule(strat, list(range(n)), plan, S.ClusterSpec())
+            m["baseline_schedule"].append([strat, n, b, schedule_to_lines(sc), sc.max_send_degree,
+                                           sc.enforce_step_bound, sc.initial_delay_s, sc.label,
+                                           [[g.group_id, list(g.member_nodes)] for g in sc.groups],
+                                           sc.step_count])
     m["transfer_step_time"] = []
     for size, b in ((26 * GB, 16), (16_060_522_496, 16), (141_107_412_992, 80)):
         plan = partition_blocks(ModelSpec("m", size, 80), b)

@@ -121,3 +121,15 @@ def test_synth_burst_matches(golden):
             for r in tr2] == misc["synth_burst_small"]
     for xs, p, want in misc["nearest_rank"]:
         assert W.nearest_rank(xs, p) == want
+
+
+def test_baseline_schedules_match(golden):
+    for strat, n, b, lines, deg, bound, delay, label, groups, steps in golden("misc")["baseline_schedule"]:
+        plan = M.partition_blocks(M.ModelSpec("m", 26 * GB, 80), b)
+        sc = S.baseline_schedule(strat, list(range(n)), plan, S.ClusterSpec())
+        assert M.schedule_to_lines(sc) == lines, (strat, n, b)
+        assert (sc.max_send_degree, sc.enforce_step_bound, sc.initial_delay_s, sc.label, sc.step_count) == \
+            (deg, bound, delay, label, steps)
+        assert [[g.group_id, list(g.member_nodes)] for g in sc.groups] == groups
+    with pytest.raises(InvalidArgumentError):
+        S.baseline_schedule("nope", [0, 1], M.partition_blocks(M.ModelSpec("m", GB, 4), 2), S.ClusterSpec())
