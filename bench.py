@@ -8,10 +8,13 @@ Llama-2-13B bf16 (26.03 GB packed image, b = 40 one-layer blocks) scaled out
 from pinned host memory (schedule node 0, the reference's MEMORY tier) to N
 GPUs with the reference's binomial λPipe schedule (n = N + 1 nodes, k = 1).
 One step = one complete scale-out: every receiver ends holding the whole
-model byte-exactly (checksummed after the timed region).
+model byte-exactly, checked EVERY step: receivers checksum each block while
+it lands (lp_mc_verify) and the sums are compared with the source manifest.
+Executor: scaleout.choose_executor — hybrid for host sources (PCIe hop as
+pinned DMA on the copy engines, NVLink relays in the multicast kernel).
 
 metric/value: aggregate delivered GB/s = N x model bytes / max-over-ranks
-device time of the multicast kernel (CUDA events on its stream).  At N >= 2
+device time of one scale-out (CUDA events around it on its stream).  At N >= 2
 the line also carries the GPU-sourced multicast (Llama-3-8B, GPU0 -> N-1
 peers, b = 16; BASELINE configs[1] at N = 8) as "gpu_source".
 
@@ -155,10 +158,14 @@ def run_reference(args):
 # our arm
 
 
-def timed_steps(so, steps, warmup, distributed, stream):
+def timed_steps(so, steps, warmup, distributed, stream, want=None):
+    """Device time per step (max over ranks).  With ``want`` (the source's
+    per-block checksums) every step's verify-as-it-lands sums are checked;
+    returns (times, all steps byte-exact, our kernel launches in timed steps
+    summed over ranks)."""
     import torch
     import torch.distributed as dist
-    times = []
+    times, ok, launches = [], True, 0
     for i in range(warmup + steps):
         if distributed:
             dist.barrier()
@@ -167,9 +174,27 @@ def timed_steps(so, steps, warmup, distributed, stream):
         t = torch.tensor([r.kernel_ms], device="cuda")
         if distributed:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if want is not None:
+            ok = ok and bool(r.checksums) and all(v == want for v in r.checksums.values())
         if i >= warmup:
             times.append(t.item())
-    return times
+            launches += r.launches
+    if distributed:
+        x = torch.tensor([launches, int(not ok)], device="cuda")
+        dist.all_reduce(x)
+        launches, ok = int(x[0].item()), x[1].item() == 0
+    return times, ok, launches
+
+
+def source_sums(so, rank, distributed, node=0):
+    """Per-block checksums of the source image (node 0), on every rank."""
+    import torch.distributed as dist
+    sums = so.checksums(node) if rank == 0 else None
+    if distributed:
+        box = [sums]
+        dist.broadcast_object_list(box, src=0)
+        sums = box[0]
+    return sums
 
 
 def main():
@@ -179,6 +204,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pull-ctas", type=int, default=64)
+    ap.add_argument("--executor", default="auto", choices=["auto", "hybrid", "kernel", "ce"],
+                    help="host-sourced scale-out executor (auto = scaleout.choose_executor)")
     ap.add_argument("--no-gpu-source", action="store_true")
     ap.add_argument("--no-serving", action="store_true")
     ap.add_argument("--requests", type=int, default=32)
@@ -209,52 +236,53 @@ def main():
     # --- main workload: C3 host -> N GPUs -----------------------------------
     plan = SO.plan_scale_out(C3_MODEL, N + 1, 1, C3_BLOCKS, host_source=True)
     M = plan.layout.weights_bytes
-    so = SO.ScaleOut(plan, distributed=distributed, tile_bytes=2 << 20, push_ctas=0, pull_ctas=args.pull_ctas,
-                     seed=SEED, device=dev, direction=1, copy_mode=0)
-    so.load_sources()
-    clocks = ClockSampler(dev)
-    clocks.start()
-    times = timed_steps(so, args.steps, args.warmup, distributed, stream)
-    clk = clocks.stop()
-    T = statistics.median(times)
-    value = N * M / (T * 1e-3) / 1e9
-    # correctness after the timed region: every receiver == the host image
-    my_nodes = so.cluster.exec_nodes
-    ok = True
-    sums = {n: so.checksums(n) for n in my_nodes}
-    allsums = [None] * world
-    if distributed:
-        dist.all_gather_object(allsums, sums)
-    else:
-        allsums = [sums]
-    merged = {}
-    for d in allsums:
-        merged.update(d)
-    host_sums = so.checksums(0) if rank == 0 else None     # the HOST node (source) image
-    if distributed:
-        box = [host_sums]
-        dist.broadcast_object_list(box, src=0)
-        host_sums = box[0]
-    ok = all(v == host_sums for v in merged.values())
+    tiles = {"hybrid": SO.HYBRID_TILE, "kernel": 2 << 20, "ce": SO.CE_TILE}
+    executor = SO.choose_executor(plan)[0] if args.executor == "auto" else args.executor
+    host_exec = {}
+    main_res = None
+    for ex in [executor] + [e for e in ("hybrid", "kernel") if e != executor]:
+        so = SO.ScaleOut(plan, distributed=distributed, tile_bytes=tiles[ex], push_ctas=0,
+                         pull_ctas=args.pull_ctas, seed=SEED, device=dev, direction=1, copy_mode=0,
+                         executor=ex, verify=True)
+        so.load_sources()
+        want = source_sums(so, rank, distributed)
+        if ex == executor:
+            clocks = ClockSampler(dev)
+            clocks.start()
+        times, ok, launches = timed_steps(so, args.steps if ex == executor else 3, args.warmup, distributed,
+                                          stream, want)
+        T = statistics.median(times)
+        host_exec[ex] = {"ms": round(T, 3), "agg_GBps": round(N * M / (T * 1e-3) / 1e9, 3), "byte_exact": ok}
+        if ex != executor:
+            so.close()
+            continue
+        clk = clocks.stop()
+        main_res = (T, ok, launches)
 
-    # --- e2e through the public API: plan + compile + launch + wait + read back
-    e2e_times = []
-    for i in range(args.warmup + args.steps):
-        if distributed:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        p2 = SO.plan_scale_out(C3_MODEL, N + 1, 1, C3_BLOCKS, host_source=True)
-        so.cluster.set_schedule(p2.schedule, p2.sources)
-        r = so.run(stream)
-        done = so.cluster.engine.complete(my_nodes[0], r.epoch)
-        assert all(done)
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-        if distributed:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        if i >= args.warmup:
-            e2e_times.append(dt.item())
-    e2e = N * M / statistics.median(e2e_times) / 1e9
+        # --- e2e through the public API: plan + compile + launch + wait + read back
+        # (the verified per-block checksums of every receiver: 8 B per block)
+        my_nodes = so.cluster.exec_nodes
+        e2e_times = []
+        for i in range(args.warmup + args.steps):
+            if distributed:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            p2 = SO.plan_scale_out(C3_MODEL, N + 1, 1, C3_BLOCKS, host_source=True)
+            so.cluster.set_schedule(p2.schedule, p2.sources)
+            r = so.run(stream)
+            assert all(v == want for v in r.checksums.values()), "e2e step delivered wrong bytes"
+            done = so.cluster.engine.complete(my_nodes[0], r.epoch)
+            assert all(done)
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            if distributed:
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            if i >= args.warmup:
+                e2e_times.append(dt.item())
+        e2e = N * M / statistics.median(e2e_times) / 1e9
+        so.close()
+    T, ok, launches = main_res
+    value = N * M / (T * 1e-3) / 1e9
     h2d = sum(plan.layout.block_lengths[int(ln.split(",")[3])] for ln in plan.lines()
               if int(ln.split(",")[1]) == 0)
 
@@ -269,20 +297,14 @@ def main():
                       "schedule_ceiling": round(M2 / src_egress, 4), "executors": {}}
         for name, kw in (("kernel", dict(executor="kernel", tile_bytes=2 << 20, pull_ctas=64, copy_mode=0)),
                          ("copy_engine", dict(executor="ce", tile_bytes=SO.CE_TILE))):
-            so2 = SO.ScaleOut(plan2, distributed=True, push_ctas=0, seed=SEED, device=dev, direction=1, **kw)
+            so2 = SO.ScaleOut(plan2, distributed=True, push_ctas=0, seed=SEED, device=dev, direction=1,
+                              verify=True, **kw)
             so2.load_sources()
-            t2 = timed_steps(so2, args.steps, args.warmup, True, stream)
+            t2, exact, _ = timed_steps(so2, args.steps, args.warmup, True, stream, source_sums(so2, rank, True))
             T2 = statistics.median(t2)
-            sums = so2.checksums(so2.cluster.exec_nodes[0])
-            src = [None]
-            if rank == 0:
-                src = [so2.checksums(0)]
-            dist.broadcast_object_list(src, src=0)
-            exact = torch.tensor([int(sums == src[0])], device="cuda")
-            dist.all_reduce(exact, op=dist.ReduceOp.MIN)
             gpu_source["executors"][name] = {
                 "ms": round(T2, 3), "agg_GBps": round((N - 1) * M2 / (T2 * 1e-3) / 1e9, 1),
-                "nvlink_roofline_frac": round(M2 / (900e9 * T2 * 1e-3), 4), "byte_exact": bool(exact.item()),
+                "nvlink_roofline_frac": round(M2 / (900e9 * T2 * 1e-3), 4), "byte_exact": exact,
                 "detail": ("in-kernel NVLink pulls (LDG.128, 64 CTAs/rank, 2 MiB tiles)" if name == "kernel" else
                            "copy engines: cuStreamWaitValue32 -> cudaMemcpyAsync -> cuStreamWriteValue32, "
                            "256 MiB tiles, no SMs")}
@@ -290,7 +312,6 @@ def main():
         best = min(gpu_source["executors"].items(), key=lambda kv: kv[1]["ms"])
         gpu_source.update({"best_executor": best[0], "ms": best[1]["ms"], "agg_GBps": best[1]["agg_GBps"],
                            "nvlink_roofline_frac": best[1]["nvlink_roofline_frac"]})
-    so.close()
 
     # --- execute-while-load serving (tokens/s + TTFT during load) ------------
     serving = None
@@ -327,7 +348,22 @@ def main():
                 cpu = {"value": round(gb, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample}
             except Exception as e:  # noqa: BLE001
                 cpu = {"value": None, "unit": "GB/s", "cores": threads, "kind": "port", "sample": f"failed: {e}"}
-        achieved = M / (T * 1e-3) / 1e9          # bytes one rank's kernel lands per launch / duration
+        achieved = M / (T * 1e-3) / 1e9          # bytes one receiver lands per step / step time
+        exec_desc = {
+            "hybrid": f"hybrid: PCIe hop as pinned DMA on the copy engines ({SO.HYBRID_TILE >> 20} MiB tiles, "
+                      f"per-tile flags), NVLink relays in the multicast kernel ({args.pull_ctas} CTAs/rank, "
+                      "LDG.128 pulls)",
+            "kernel": f"in-kernel PCIe/NVLink pulls (LDG.128, {args.pull_ctas} CTAs/rank, 2 MiB tiles)",
+            "ce": "copy engines only (256 MiB tiles)"}[executor]
+        if executor == "kernel":
+            traffic, tnote = int(NCU_TRAFFIC_RATIO * M), (
+                "dram read+write per launch from ncu --set full of the same kernel "
+                "(profiles/mc_kernel_host_pull_full_r01.csv: 3.163 GB for a 3.193 GB image, ratio 0.991) "
+                "scaled to this image")
+        else:
+            traffic, tnote = None, (
+                "the PCIe hop is copy-engine DMA, not an SM kernel; the in-kernel PCIe pull executor's ncu "
+                "traffic is 0.991 x image bytes (profiles/mc_kernel_host_pull_full_r01.csv)")
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(T, 3), "higher_is_better": True, "scaling": "weak",
@@ -335,7 +371,11 @@ def main():
             "config": {"workload": f"{C3_MODEL} bf16 ({M / 1e9:.2f} GB) scale-out from pinned host memory "
                                    f"to {N} GPU(s), b={C3_BLOCKS}, k=1, reference binomial schedule "
                                    f"({plan.schedule.step_count} steps)",
-                       "executor": f"in-kernel PCIe/NVLink pulls (LDG.128, {args.pull_ctas} CTAs/rank, 2 MiB tiles)",
+                       "executor": exec_desc,
+                       "host_executors": host_exec,
+                       "verify": "every step: receivers checksum each block while it lands (lp_mc_verify, "
+                                 "32 CTAs on a side stream) and the sums are read back and compared with the "
+                                 "source manifest",
                        "l2": "inputs larger than L2 (26 GB image per step)",
                        "parallelism": f"{N} GPU ranks, one process per GPU"},
             "scale_out_ms": round(T, 3), "byte_exact": ok,
@@ -343,14 +383,12 @@ def main():
                          "peak": 64.0, "unit": "GB/s", "frac": round(achieved / 64.0, 4),
                          "peak_note": "PCIe Gen5 x16 nominal (the reference's h2d_Bps); measured DMA H2D on "
                                       "this pool 55.6 GB/s (profiles/probe_r01.json)",
-                         "traffic": int(NCU_TRAFFIC_RATIO * M),
-                         "traffic_note": "dram read+write per launch from ncu --set full of the same kernel "
-                                         "(profiles/mc_kernel_host_pull_full_r01.csv: 3.163 GB for a 3.193 GB "
-                                         "image, ratio 0.991) scaled to this image"},
+                         "traffic": traffic, "traffic_note": tnote},
             "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(4 * plan.block_count * N),
-                    "path": "paper_2502_09922_b200.scaleout: plan_scale_out + set_schedule + run + completion readback"},
-            "gpu_launches": args.steps * N,
+                    "d2h_bytes_per_step": int(12 * plan.block_count * N),
+                    "path": "paper_2502_09922_b200.scaleout: plan_scale_out + set_schedule + run (verified "
+                            "checksums read back) + completion readback"},
+            "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,
             "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops")},

@@ -123,8 +123,28 @@ int lp_mc_configure(lp_mc* mc, int direction, int push_mode, int pull_mode, int6
  * streams on the device), else a parked wait stalls unrelated streams. */
 int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
                  void* const* block_events);
+/* Hybrid executor (option host_dma = 1): the transfers whose sender is a HOST
+ * node leave the kernel's op lists and are enqueued here, per receiving GPU
+ * node, on the copy engines (pinned-host DMA over PCIe, per-tile flag writes);
+ * lp_mc_run on another stream of the same device relays the landed tiles over
+ * NVLink, waiting on those flags.  Replaces the h2d leg of the reference's
+ * step cost (simengine.py:95-103, h2d_Bps) with real pinned DMA overlapped
+ * with the GPU->GPU relay. */
+int lp_mc_run_host_dma(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
+                       void* const* block_events);
+/* Verify-as-it-lands: zero sums_dev[n_blocks] (device memory) and launch
+ * `ctas` CTAs on `stream` that checksum every block `node` receives this
+ * epoch, tile by tile as its flags publish (either executor), with the
+ * lp_block_checksums function; entries of blocks the node does not receive
+ * stay 0.  Run it on a stream other than the multicast's. */
+int lp_mc_verify(lp_mc* mc, int node, uint32_t epoch, int ctas, uint64_t* sums_dev, void* stream);
+/* number of ops node executes in-kernel (push + pull roles) and on the host
+ * DMA path (0 unless host_dma) under the current configuration */
+int lp_mc_node_ops(lp_mc* mc, int node, int* kernel_ops, int* dma_ops);
 /* tunables: "wide_loads" (0/1: 256 B L2 fetch granule on LDG-role loads),
- * "window" (1..8), "timeout_ms" (flag-wait watchdog, default 20000) */
+ * "window" (1..8), "timeout_ms" (flag-wait watchdog, default 20000),
+ * "host_dma" (0/1: HOST-sourced transfers on the copy engines, see
+ * lp_mc_run_host_dma) */
 int lp_mc_set_option(lp_mc* mc, const char* name, int64_t value);
 /* synchronise `stream`; code = 1 (and return -3) if a flag wait timed out */
 int lp_mc_status(lp_mc* mc, void* stream, int* code);

@@ -50,7 +50,7 @@ struct OpDev {
   int32_t block, src, dst, wait, step, pad;
 };
 struct ExecDesc {
-  int32_t node, push_b, push_e, pull_b, pull_e, recv_b, recv_e, pad;
+  int32_t node, push_b, push_e, pull_b, pull_e, recv_b, recv_e, dma_b, dma_e, pad;
 };
 struct McParams {
   const NodeDev* nodes;
@@ -70,13 +70,13 @@ struct McParams {
 };
 
 __device__ __forceinline__ bool wait_flag(const uint32_t* f, uint32_t epoch, uint64_t t0,
-                                          uint64_t timeout_ns, int* err) {
+                                          uint64_t timeout_ns, int* err, int code = 1) {
   uint32_t spins = 0;
   while (lp::ld_acquire_sys(f) != epoch) {
     if (++spins > 64) {
       lp::nanosleep(200);
       if ((spins & 1023) == 0 && lp::globaltimer() - t0 > timeout_ns) {
-        atomicExch(err, 1);
+        atomicExch(err, code);
         return false;
       }
     }
@@ -378,6 +378,84 @@ __global__ void __launch_bounds__(LP_MC_THREADS) mc_kernel(const McParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Verify-as-it-lands: per-block checksums (the lp_block_checksums function,
+// sum of mix64(word ^ k * golden) over the block's 8-byte words) of what a
+// receiver holds, computed tile by tile while the scale-out is still running.
+// Every received block is cut into pieces inside its tiles; piece g goes to
+// CTA g % gridDim.x, which waits for the tile's flag (written by the kernel
+// or the copy-engine executor alike) and folds the piece into sums[block].
+struct VerifyParams {
+  NodeDev me;
+  const BlockDev* blocks;
+  const int32_t* order;   // blocks in this node's receive (step) order
+  unsigned long long* sums;
+  int* err;
+  int64_t tile_bytes, piece_bytes;
+  uint64_t timeout_ns;
+  uint32_t epoch;
+  int n_order;
+};
+
+__global__ void __launch_bounds__(256) verify_kernel(const VerifyParams p) {
+  __shared__ uint64_t part[8];
+  __shared__ int s_ok;
+  const uint64_t t0 = lp::globaltimer();
+  if (threadIdx.x == 0) s_ok = 1;
+  int64_t g = 0;
+  for (int o = 0; o < p.n_order; ++o) {
+    const int blk = p.order[o];
+    const BlockDev bl = p.blocks[blk];
+    for (int t = 0; t < bl.ntiles; ++t) {
+      const int64_t tlo = (int64_t)t * p.tile_bytes;
+      const int64_t tlen = min(p.tile_bytes, bl.len - tlo);
+      const int64_t np = (tlen + p.piece_bytes - 1) / p.piece_bytes;
+      const int64_t first = (blockIdx.x - g % gridDim.x + gridDim.x) % gridDim.x;  // my first piece here
+      g += np;
+      if (first >= np) continue;
+      __syncthreads();
+      if (threadIdx.x == 0 && !wait_flag(p.me.flags + bl.tile_base + t, p.epoch, t0, p.timeout_ns, p.err, 2))
+        s_ok = 0;
+      __syncthreads();
+      if (!s_ok) return;
+      uint64_t acc = 0;
+      constexpr uint64_t G = 0x9E3779B97F4A7C15ull;
+      for (int64_t q = first; q < np; q += gridDim.x) {
+        const int64_t lo = tlo + q * p.piece_bytes;
+        const int64_t n16 = min(p.piece_bytes, tlen - q * p.piece_bytes) >> 4;   // pieces are 16 B multiples
+        const ulonglong2* w = reinterpret_cast<const ulonglong2*>(p.me.image + bl.off + lo);
+        const uint64_t k0 = (uint64_t)(lo >> 3);
+        const int T = blockDim.x;
+        int64_t i = threadIdx.x;
+        for (; i + 3 * T < n16; i += 4 * T) {   // 64 B in flight per thread
+          ulonglong2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = __ldcs(w + i + u * T);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint64_t k = k0 + 2 * (uint64_t)(i + u * T);
+            acc += lp::mix64(v[u].x ^ (k * G)) + lp::mix64(v[u].y ^ ((k + 1) * G));
+          }
+        }
+        for (; i < n16; i += T) {
+          const ulonglong2 v = __ldcs(w + i);
+          const uint64_t k = k0 + 2 * (uint64_t)i;
+          acc += lp::mix64(v.x ^ (k * G)) + lp::mix64(v.y ^ ((k + 1) * G));
+        }
+      }
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+      if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint64_t sum = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) sum += part[i];
+        atomicAdd(p.sums + blk, (unsigned long long)sum);
+      }
+    }
+  }
+}
+
 }  // namespace
 
 struct lp_mc {
@@ -393,6 +471,8 @@ struct lp_mc {
   // compiled per-node op ranges
   std::vector<ExecDesc> per_node;
   std::vector<OpDev> h_ops;         // host copy of the compiled op lists (copy-engine executor)
+  std::vector<int32_t> vr_off;      // [N+1] offsets of each node's receive order in d_vorder
+  int32_t* d_vorder = nullptr;
   int dev = 0;
   NodeDev* d_nodes = nullptr;
   BlockDev* d_blocks = nullptr;
@@ -405,6 +485,7 @@ struct lp_mc {
   int64_t chunk_bytes = 16384;
   int window = 3;
   int wide_loads = 0;
+  int host_dma = 0;                   // HOST-sourced transfers run on the copy engines (lp_mc_run_host_dma)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;   // flag-wait watchdog
   cudaStream_t poll = nullptr;   // private non-blocking stream for host polls
 };
@@ -463,7 +544,11 @@ static int compile(lp_mc* mc) {
   }
   // executor of a transfer: its sender pushes (direction 0) unless the sender
   // is a HOST node; with direction 1 every transfer is pulled by its receiver
-  auto pulled = [&](const Row& r) { return mc->direction == 1 || mc->nodes[r.snd].kind == LP_NODE_HOST; };
+  auto from_host = [&](const Row& r) { return mc->nodes[r.snd].kind == LP_NODE_HOST; };
+  auto pulled = [&](const Row& r) { return mc->direction == 1 || from_host(r); };
+  // with host_dma the receiver's copy engine performs the PCIe hop and the
+  // kernel only relays over NVLink (waiting on the flags the DMA publishes)
+  auto dma = [&](const Row& r) { return mc->host_dma && from_host(r); };
   std::vector<OpDev> ops;
   std::vector<int32_t> recv;
   mc->per_node.assign(N, ExecDesc{});
@@ -476,15 +561,34 @@ static int compile(lp_mc* mc) {
     d.push_e = (int)ops.size();
     d.pull_b = (int)ops.size();
     for (const Row& r : rows)
-      if (r.rcv == n && pulled(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1, r.step, 0});
+      if (r.rcv == n && pulled(r) && !dma(r))
+        ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1, r.step, 0});
     d.pull_e = (int)ops.size();
+    d.dma_b = (int)ops.size();
+    for (const Row& r : rows)
+      if (r.rcv == n && dma(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, 0, r.step, 0});
+    d.dma_e = (int)ops.size();
     // tiles other nodes push into n: waited for before n's kernel completes
     d.recv_b = (int)recv.size();
     for (const Row& r : rows)
       if (r.rcv == n && !pulled(r)) recv.push_back(r.blk);
     d.recv_e = (int)recv.size();
   }
+  // receive order per node (verify kernel): blocks in the step order they land
+  std::vector<int32_t> vorder;
+  mc->vr_off.assign(N + 1, 0);
+  for (int n = 0; n < N; ++n) {
+    mc->vr_off[n] = (int)vorder.size();
+    for (const Row& r : rows)
+      if (r.rcv == n) vorder.push_back(r.blk);
+  }
+  mc->vr_off[N] = (int)vorder.size();
   LP_CUDA(cudaSetDevice(mc->dev));
+  if (mc->d_vorder) cudaFree(mc->d_vorder);
+  mc->d_vorder = nullptr;
+  LP_CUDA(cudaMalloc(&mc->d_vorder, sizeof(int32_t) * std::max<size_t>(1, vorder.size())));
+  if (!vorder.empty())
+    LP_CUDA(cudaMemcpy(mc->d_vorder, vorder.data(), sizeof(int32_t) * vorder.size(), cudaMemcpyHostToDevice));
   if (mc->d_ops) cudaFree(mc->d_ops);
   if (mc->d_recv) cudaFree(mc->d_recv);
   mc->d_ops = nullptr;
@@ -536,6 +640,12 @@ int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_of
   }
   cudaMemcpy(mc->d_blocks, mc->blocks.data(), sizeof(BlockDev) * n_blocks, cudaMemcpyHostToDevice);
   cudaMemset(mc->d_err, 0, sizeof(int));
+  // force-load the spinning kernels now: under lazy module loading, loading a
+  // kernel while another one spins on its flags would wait for that one
+  // (multicast kernel <-> verify kernel <-> copy-engine flags deadlock)
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, mc_kernel);
+  cudaFuncGetAttributes(&fa, verify_kernel);
   *out = mc;
   return 0;
 }
@@ -547,6 +657,7 @@ int lp_mc_destroy(lp_mc* mc) {
   cudaFree(mc->d_blocks);
   cudaFree(mc->d_ops);
   cudaFree(mc->d_recv);
+  cudaFree(mc->d_vorder);
   cudaFree(mc->d_err);
   if (mc->poll) cudaStreamDestroy(mc->poll);
   delete mc;
@@ -617,6 +728,9 @@ int lp_mc_set_option(lp_mc* mc, const char* name, int64_t value) {
   } else if (!strcmp(name, "window")) {
     LP_CHECK(value >= 1 && value <= kMaxWindow, "lp_mc_set_option: window must be in [1, %d]", kMaxWindow);
     mc->window = (int)value;
+  } else if (!strcmp(name, "host_dma")) {
+    if ((value != 0) != (mc->host_dma != 0)) mc->dirty = true;
+    mc->host_dma = value != 0;
   } else if (!strcmp(name, "timeout_ms")) {
     LP_CHECK(value > 0, "lp_mc_set_option: timeout_ms must be positive");
     mc->timeout_ns = (uint64_t)value * 1000000ull;
@@ -702,6 +816,48 @@ static int resolve_stream_memops() {
 #define cuStreamWaitValue32 g_wait32
 #define cuStreamWriteValue32 g_write32
 
+// Enqueue ops `seq` (indices into h_ops) of `node` on the copy engines.
+static int enqueue_ce(lp_mc* mc, int node, uint32_t epoch, const std::vector<int>& seq, int n_streams,
+                      void* const* streams, void* const* block_events) {
+  int k = 0;
+  const bool dbg = getenv("LP_DEBUG_CE") != nullptr;
+  for (int oi : seq) {
+    const OpDev op = mc->h_ops[oi];
+    if (dbg)
+      fprintf(stderr, "lp_mc ce node %d: op %d step %d %d->%d block %d wait %d stream %d\n", node, oi, op.step,
+              op.src, op.dst, op.block, op.wait, k % n_streams);
+    const BlockDev bl = mc->blocks[op.block];
+    const NodeDev src = mc->nodes[op.src];
+    const NodeDev dst = mc->nodes[op.dst];
+    CUstream s = (CUstream)streams[k % n_streams];
+    for (int t = 0; t < bl.ntiles; ++t) {
+      const int64_t lo = (int64_t)t * mc->tile_bytes;
+      const int64_t n = std::min<int64_t>(mc->tile_bytes, bl.len - lo);
+      if (op.wait) {
+        CUresult r = cuStreamWaitValue32(s, (CUdeviceptr)(src.flags + bl.tile_base + t), epoch,
+                                         CU_STREAM_WAIT_VALUE_GEQ);
+        LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWaitValue32 failed (%d)", (int)r);
+      }
+      LP_CUDA(cudaMemcpyAsync(dst.image + bl.off + lo, src.image + bl.off + lo, (size_t)n, cudaMemcpyDefault,
+                              (cudaStream_t)s));
+      CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.flags + bl.tile_base + t), epoch,
+                                        CU_STREAM_WRITE_VALUE_DEFAULT);
+      LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
+    }
+    CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.counts + op.block), epoch * (uint32_t)bl.ntiles,
+                                      CU_STREAM_WRITE_VALUE_DEFAULT);
+    LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
+    if (dst.ready) {
+      r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.ready + op.block), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+      LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: ready write failed (%d)", (int)r);
+    }
+    if (block_events && block_events[op.block] && op.dst == node)
+      LP_CUDA(cudaEventRecord((cudaEvent_t)block_events[op.block], (cudaStream_t)s));
+    ++k;
+  }
+  return 0;
+}
+
 int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
                  void* const* block_events) {
   if (resolve_stream_memops() != 0) return -1;
@@ -713,53 +869,68 @@ int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const
   // direction 1: this node's copy engine pulls every block it receives;
   // direction 0: its copy engine pushes every block it sends (waits are then
   // on its OWN flags, flag writes land in the receiver's memory) and it still
-  // pulls host-sourced blocks.  Both run in schedule step order.
-  // one step-ordered sequence of this node's pushes and pulls: a push of a
-  // block this node itself pulls (e.g. from the host) must be enqueued after
-  // that pull, or a single stream would wait on itself
+  // pulls host-sourced blocks.  One step-ordered sequence of this node's
+  // pushes and pulls: a push of a block this node itself pulls (e.g. from the
+  // host) must be enqueued after that pull, or a single stream would wait on
+  // itself.
   std::vector<int> seq;
   for (int oi = ex.push_b; oi < ex.push_e; ++oi) seq.push_back(oi);
   for (int oi = ex.pull_b; oi < ex.pull_e; ++oi) seq.push_back(oi);
+  for (int oi = ex.dma_b; oi < ex.dma_e; ++oi) seq.push_back(oi);
   std::stable_sort(seq.begin(), seq.end(),
                    [&](int a, int b) { return mc->h_ops[a].step < mc->h_ops[b].step; });
-  int k = 0;
-  const bool dbg = getenv("LP_DEBUG_CE") != nullptr;
-  for (int oi : seq) {
-    {
-      const OpDev op = mc->h_ops[oi];
-      if (dbg)
-        fprintf(stderr, "lp_mc_run_ce node %d: op %d step %d %d->%d block %d wait %d stream %d\n", node, oi, op.step,
-                op.src, op.dst, op.block, op.wait, k % n_streams);
-      const BlockDev bl = mc->blocks[op.block];
-      const NodeDev src = mc->nodes[op.src];
-      const NodeDev dst = mc->nodes[op.dst];
-      CUstream s = (CUstream)streams[k % n_streams];
-      for (int t = 0; t < bl.ntiles; ++t) {
-        const int64_t lo = (int64_t)t * mc->tile_bytes;
-        const int64_t n = std::min<int64_t>(mc->tile_bytes, bl.len - lo);
-        if (op.wait) {
-          CUresult r = cuStreamWaitValue32(s, (CUdeviceptr)(src.flags + bl.tile_base + t), epoch,
-                                           CU_STREAM_WAIT_VALUE_GEQ);
-          LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWaitValue32 failed (%d)", (int)r);
-        }
-        LP_CUDA(cudaMemcpyAsync(dst.image + bl.off + lo, src.image + bl.off + lo, (size_t)n, cudaMemcpyDefault,
-                                (cudaStream_t)s));
-        CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.flags + bl.tile_base + t), epoch,
-                                          CU_STREAM_WRITE_VALUE_DEFAULT);
-        LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
-      }
-      CUresult r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.counts + op.block), epoch * (uint32_t)bl.ntiles,
-                                        CU_STREAM_WRITE_VALUE_DEFAULT);
-      LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: cuStreamWriteValue32 failed (%d)", (int)r);
-      if (dst.ready) {
-        r = cuStreamWriteValue32(s, (CUdeviceptr)(dst.ready + op.block), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
-        LP_CHECK(r == CUDA_SUCCESS, "lp_mc_run_ce: ready write failed (%d)", (int)r);
-      }
-      if (block_events && block_events[op.block] && op.dst == node)
-        LP_CUDA(cudaEventRecord((cudaEvent_t)block_events[op.block], (cudaStream_t)s));
-    }
-    ++k;
-  }
+  return enqueue_ce(mc, node, epoch, seq, n_streams, streams, block_events);
+}
+
+// Hybrid executor, PCIe half: with option host_dma=1 the transfers whose
+// sender is a HOST node are left out of the kernel's op lists; this enqueues
+// them (this node's host pulls, in step order) on the copy engines, while
+// lp_mc_run on another stream relays the landed tiles over NVLink.
+int lp_mc_run_host_dma(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
+                       void* const* block_events) {
+  if (resolve_stream_memops() != 0) return -1;
+  LP_CHECK(mc && node >= 0 && node < mc->n_nodes, "lp_mc_run_host_dma: bad node");
+  LP_CHECK(epoch >= 1 && n_streams >= 1 && streams, "lp_mc_run_host_dma: bad arguments");
+  LP_CHECK(mc->host_dma, "lp_mc_run_host_dma: enable option host_dma first");
+  if (mc->dirty && compile(mc) != 0) return -2;
+  const ExecDesc ex = mc->per_node[node];
+  std::vector<int> seq;
+  for (int oi = ex.dma_b; oi < ex.dma_e; ++oi) seq.push_back(oi);
+  return enqueue_ce(mc, node, epoch, seq, n_streams, streams, block_events);
+}
+
+// Ops the kernel (push + pull roles) and the host DMA would execute for node.
+int lp_mc_node_ops(lp_mc* mc, int node, int* kernel_ops, int* dma_ops) {
+  LP_CHECK(mc && node >= 0 && node < mc->n_nodes && kernel_ops && dma_ops, "lp_mc_node_ops: bad arguments");
+  if (mc->dirty && compile(mc) != 0) return -2;
+  const ExecDesc ex = mc->per_node[node];
+  *kernel_ops = (ex.push_e - ex.push_b) + (ex.pull_e - ex.pull_b);
+  *dma_ops = ex.dma_e - ex.dma_b;
+  return 0;
+}
+
+int lp_mc_verify(lp_mc* mc, int node, uint32_t epoch, int ctas, uint64_t* sums_dev, void* stream) {
+  LP_CHECK(mc && node >= 0 && node < mc->n_nodes && sums_dev, "lp_mc_verify: bad arguments");
+  LP_CHECK(epoch >= 1 && ctas >= 1 && ctas <= 1024, "lp_mc_verify: bad epoch / CTA count");
+  LP_CHECK(mc->nodes[node].kind == LP_NODE_GPU && mc->nodes[node].flags,
+           "lp_mc_verify: node %d is not a GPU node with signals", node);
+  if (mc->dirty && compile(mc) != 0) return -2;
+  LP_CUDA(cudaMemsetAsync(sums_dev, 0, sizeof(uint64_t) * mc->n_blocks, (cudaStream_t)stream));
+  const int nb = mc->vr_off[node + 1] - mc->vr_off[node];
+  if (nb == 0) return 0;
+  VerifyParams p{};
+  p.me = mc->nodes[node];
+  p.blocks = mc->d_blocks;
+  p.order = mc->d_vorder + mc->vr_off[node];
+  p.sums = reinterpret_cast<unsigned long long*>(sums_dev);
+  p.err = mc->d_err;
+  p.tile_bytes = mc->tile_bytes;
+  p.piece_bytes = std::min<int64_t>(mc->tile_bytes, 1 << 20);
+  p.timeout_ns = mc->timeout_ns;
+  p.epoch = epoch;
+  p.n_order = nb;
+  verify_kernel<<<ctas, 256, 0, (cudaStream_t)stream>>>(p);
+  LP_CUDA(cudaGetLastError());
   return 0;
 }
 
@@ -771,7 +942,8 @@ int lp_mc_status(lp_mc* mc, void* stream, int* code) {
   *code = h;
   if (h) {
     cudaMemset(mc->d_err, 0, sizeof(int));
-    lp::set_error("lp_mc: watchdog expired waiting for a tile flag (a peer never delivered)");
+    lp::set_error("lp_mc: watchdog expired waiting for a tile flag (a peer never delivered; %s)",
+                  h == 2 ? "verify kernel" : "multicast kernel");
     return -3;
   }
   return 0;

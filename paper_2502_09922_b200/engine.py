@@ -118,6 +118,26 @@ class MulticastEngine:
             evs = (C.c_void_p * self.n_blocks)(*[int(e) if e else None for e in block_events])
         N.call("lp_mc_run_ce", self._h, node, epoch, len(streams), arr, evs)
 
+    def run_host_dma(self, node: int, epoch: int, streams: list, block_events: list | None = None):
+        """Enqueue ``node``'s HOST-sourced receives on copy engines (hybrid
+        executor, option host_dma = 1; see lp_mc_run_host_dma)."""
+        arr = (C.c_void_p * len(streams))(*[int(x) for x in streams])
+        evs = None
+        if block_events is not None:
+            evs = (C.c_void_p * self.n_blocks)(*[int(e) if e else None for e in block_events])
+        N.call("lp_mc_run_host_dma", self._h, node, epoch, len(streams), arr, evs)
+
+    def verify(self, node: int, epoch: int, sums_ptr: int, stream: int = 0, ctas: int = 32):
+        """Checksum ``node``'s received blocks as they land (lp_mc_verify)
+        into ``n_blocks`` uint64 at device pointer ``sums_ptr``."""
+        N.call("lp_mc_verify", self._h, node, epoch, ctas, C.c_void_p(sums_ptr), C.c_void_p(stream or None))
+
+    def node_ops(self, node: int) -> tuple:
+        """(in-kernel ops, host-DMA ops) ``node`` executes."""
+        k, d = C.c_int(), C.c_int()
+        N.call("lp_mc_node_ops", self._h, node, C.byref(k), C.byref(d))
+        return k.value, d.value
+
     def status(self, stream: int = 0) -> None:
         code = C.c_int()
         N.call("lp_mc_status", self._h, C.c_void_p(stream or None), C.byref(code))
@@ -476,6 +496,35 @@ class Cluster:
                     st.wait_event(after)
             self.engine.run_ce(node, epoch, [st.cuda_stream for st in streams])
         return epoch
+
+    def launch_hybrid(self, stream, push_ctas: int = 0, pull_ctas: int = 64, epoch: int | None = None) -> tuple:
+        """One epoch with the hybrid executor: every exec node's HOST-sourced
+        receives run as pinned DMA on its copy-engine stream, the NVLink relays
+        run in the multicast kernel on ``stream`` (only launched when the node
+        has kernel ops).  ``stream`` (torch stream) ends up waiting for both.
+        Returns (epoch, kernel launches)."""
+        import torch
+        if epoch is None:
+            self.epoch += 1
+            epoch = self.epoch
+        else:
+            self.epoch = epoch
+        self.engine.set_option("host_dma", 1)
+        start = torch.cuda.Event()
+        start.record(stream)
+        run_kernel = []
+        for node in self.exec_nodes:
+            k_ops, d_ops = self.engine.node_ops(node)
+            if d_ops:
+                (st,) = self.ce_streams(node, 1)
+                st.wait_event(start)
+                self.engine.run_host_dma(node, epoch, [st.cuda_stream])
+            if k_ops:
+                run_kernel.append(node)
+        if run_kernel:
+            self.engine.run(run_kernel, epoch, push_ctas, pull_ctas, stream.cuda_stream)
+        self.join_ce(stream)
+        return epoch, int(bool(run_kernel))
 
     def join_ce(self, stream) -> None:
         """Make ``stream`` wait for every CE stream of this process."""

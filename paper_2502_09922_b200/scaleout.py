@@ -90,15 +90,20 @@ def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
 
 
 CE_TILE = 256 << 20
+HYBRID_TILE = 64 << 20   # DMA tile of the PCIe hop = relay granule of the kernel
 
 
 def choose_executor(plan: ScaleOutPlan, tile_bytes: int = E.DEFAULT_TILE):
     """Measured policy (profiles/mc_sweeps_r01.md, p2p_micro_r01.txt):
-    GPU-sourced schedules with relays (>= 3 nodes) run on the copy engines
-    with 256 MiB tiles — DMA keeps ~778 GB/s per direction while a relay
-    sends and receives, SM-issued NVLink traffic drops to ~673 GB/s —
-    everything else (host sources, 1 -> 1) runs in-kernel (2 MiB tiles)."""
-    if not plan.host_source and len(plan.nodes) >= 3 and plan.block_count <= 32:
+    host-sourced schedules run hybrid — the PCIe hop as pinned DMA on the
+    copy engines (55.3 GB/s vs 51.4 GB/s for SM-issued PCIe reads), NVLink
+    relays in the kernel; GPU-sourced schedules with relays (>= 3 nodes) run
+    on the copy engines with 256 MiB tiles — DMA keeps ~778 GB/s per
+    direction while a relay sends and receives, SM-issued NVLink traffic
+    drops to ~673 GB/s — everything else (1 -> 1) runs in-kernel."""
+    if plan.host_source:
+        return "hybrid", HYBRID_TILE
+    if len(plan.nodes) >= 3 and plan.block_count <= 32:
         return "ce", CE_TILE
     # long schedules (e.g. Llama-3-70B, b = 80: 81 serial ops per relay) lose
     # more to tile-granular waits on the copy engines than they gain: measured
@@ -112,6 +117,8 @@ class ScaleOutResult:
     kernel_ms: float                 # device time of this rank's multicast kernel
     wall_ms: float                   # host wall time launch -> complete
     arrivals_ms: dict = field(default_factory=dict)   # node -> [per-block arrival, ms from start]
+    checksums: dict = field(default_factory=dict)     # node -> per-block checksums (verify=True)
+    launches: int = 0                                  # our kernels launched by this run (this process)
 
 
 class ScaleOut:
@@ -119,7 +126,8 @@ class ScaleOut:
 
     def __init__(self, plan: ScaleOutPlan, distributed: bool = False, tile_bytes: int = E.DEFAULT_TILE,
                  push_ctas: int = 0, pull_ctas: int = 64, seed: int = 0, device: int = 0, direction: int = 1,
-                 copy_mode: int = 1, chunk_bytes: int = 16384, executor: str = "kernel", ce_streams: int = 1):
+                 copy_mode: int = 1, chunk_bytes: int = 16384, executor: str = "kernel", ce_streams: int = 1,
+                 verify: bool = False, verify_ctas: int = 32):
         self.plan = plan
         self.distributed = distributed
         self.push_ctas, self.pull_ctas = push_ctas, pull_ctas
@@ -133,11 +141,18 @@ class ScaleOut:
             n_gpu = len(plan.nodes) - (1 if plan.host_source else 0)
             self.cluster = E.Cluster.local(n_gpu, lay.block_offsets, lay.block_lengths, lay.weights_bytes,
                                            device=device, host_node=plan.host_source, tile_bytes=tile_bytes)
-        if executor not in ("kernel", "ce"):
-            raise ValueError("executor is 'kernel' (in-kernel NVLink/PCIe copies), 'ce' (copy engines) or 'auto'")
+        if executor not in ("kernel", "ce", "hybrid"):
+            raise ValueError("executor is 'kernel' (in-kernel NVLink/PCIe copies), 'ce' (copy engines), "
+                             "'hybrid' (host DMA + in-kernel relay) or 'auto'")
         self.executor = executor
         self.ce_streams = ce_streams
         self.cluster.engine.configure(direction, copy_mode, copy_mode, chunk_bytes, 3)
+        self.cluster.engine.set_option("host_dma", int(executor == "hybrid"))
+        self.kernel_launches = 0      # multicast kernels of the last run (this process)
+        # verify-as-it-lands (lp_mc_verify): receivers checksum every block
+        # while it streams in; run() returns the sums (a d2h of 8 B per block)
+        self.verify, self.verify_ctas = verify, verify_ctas
+        self._vbuf = {}
         self.seed = seed
         self.device = device
         self._loaded = False
@@ -168,19 +183,61 @@ class ScaleOut:
         t0 = time.perf_counter()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(s)
+        vnodes = [n for n in self.cluster.exec_nodes if n not in self.plan.sources] if self.verify else []
+        vstreams = []
+        for node in vnodes:
+            if node not in self._vbuf:
+                self._vbuf[node] = (torch.zeros(self.plan.block_count, dtype=torch.int64, device=s.device),
+                                    torch.empty(self.plan.block_count, dtype=torch.int64, pin_memory=True),
+                                    torch.cuda.Stream(device=s.device))
+            vs = self._vbuf[node][2]
+            vs.wait_event(ev0)
+            vstreams.append((node, vs))
+        epoch_next = self.cluster.epoch + 1
+        for node, vs in vstreams:   # launched first: they park on the tile flags of this epoch
+            self.cluster.engine.verify(node, epoch_next, self._vbuf[node][0].data_ptr(), vs.cuda_stream,
+                                       self.verify_ctas)
         if self.executor == "ce":
             if not self._loaded:
                 self.load_sources()
             epoch = self.cluster.launch_ce(self.ce_streams, after=ev0)
             self.cluster.join_ce(s)
+            for node, vs in vstreams:
+                ev = torch.cuda.Event()
+                ev.record(vs)
+                s.wait_event(ev)
+            self._readback(vstreams, s)
             ev1.record(s)
             s.synchronize()
+            self.kernel_launches = 0
+        elif self.executor == "hybrid":
+            if not self._loaded:
+                self.load_sources()
+            epoch, self.kernel_launches = self.cluster.launch_hybrid(s, self.push_ctas, self.pull_ctas)
         else:
+            self.kernel_launches = 1
             epoch = self.launch(sp)
+        if self.executor != "ce":
+            for node, vs in vstreams:
+                ev = torch.cuda.Event()
+                ev.record(vs)
+                s.wait_event(ev)
+            self._readback(vstreams, s)
             ev1.record(s)
             self.cluster.wait(sp)
+        sums = {}
+        for node, _ in vstreams:
+            sums[node] = [int(x) & 0xFFFFFFFFFFFFFFFF for x in self._vbuf[node][1].tolist()]
+        assert epoch == epoch_next
         wall = (time.perf_counter() - t0) * 1e3
-        return ScaleOutResult(epoch, ev0.elapsed_time(ev1), wall)
+        return ScaleOutResult(epoch, ev0.elapsed_time(ev1), wall, checksums=sums,
+                              launches=self.kernel_launches + len(vstreams))
+
+    def _readback(self, vstreams, s):
+        import torch
+        with torch.cuda.stream(s):
+            for node, _ in vstreams:
+                self._vbuf[node][1].copy_(self._vbuf[node][0], non_blocking=True)
 
     def arrivals(self, node: int) -> list:
         return self.cluster.engine.arrivals_ns(node)

@@ -59,6 +59,11 @@ def run_case(n, k, b, host, tile, push, pull, oracle_sums, epochs=2, push_mode=1
                 cl.launch_ce(1, after=ev)
                 cl.join_ce(torch.cuda.current_stream())
                 torch.cuda.synchronize()
+            elif executor == "hybrid":
+                import torch
+                cl.engine.set_option("host_dma", 1)
+                cl.launch_hybrid(torch.cuda.current_stream(), push_ctas=push, pull_ctas=pull)
+                cl.wait(torch.cuda.current_stream().cuda_stream)
             else:
                 cl.launch(push_ctas=push, pull_ctas=pull)
                 cl.wait()
@@ -69,7 +74,7 @@ def run_case(n, k, b, host, tile, push, pull, oracle_sums, epochs=2, push_mode=1
                 assert got == want, (n, k, b, host, ep, i)
             for i in nodes[k:]:
                 assert all(cl.engine.complete(i, cl.epoch))
-                if executor == "kernel":      # the CE executor records arrivals as events instead
+                if executor == "kernel":      # copy-engine ops record no arrival timestamps
                     arr = cl.engine.arrivals_ns(i)
                     assert all(a > 0 for a in arr)
     finally:
@@ -106,6 +111,16 @@ def test_multicast_delivers_source_bytes(n, k, b, host, tile, push, pull, direct
 @pytest.mark.parametrize("direction", [0, 1])
 def test_copy_engine_executor_delivers_source_bytes(n, k, b, host, tile, direction, oracle_sums):
     run_case(n, k, b, host, tile, 0, 1, oracle_sums, direction=direction, executor="ce", chunk=min(16384, tile))
+
+
+@pytest.mark.parametrize("n,k,b,tile", [(2, 1, 8, 1 << 20), (3, 1, 8, 512 * 1024), (5, 1, 8, 1 << 20),
+                                         (9, 1, 8, 2 << 20), (9, 2, 8, 1 << 20), (5, 1, 1, 4096)])
+@pytest.mark.parametrize("direction", [0, 1])
+def test_hybrid_executor_delivers_source_bytes(n, k, b, tile, direction, oracle_sums):
+    """Host hop on the copy engines, NVLink relays in the kernel (host_dma)."""
+    push, pull = (4, 0) if direction == 0 else (0, 8)
+    run_case(n, k, b, True, tile, push, pull, oracle_sums, direction=direction, executor="hybrid",
+             chunk=min(16384, tile))
 
 
 def test_engine_rejects_bad_schedules():

@@ -1,0 +1,65 @@
+"""GPU parity of the ``scale_out`` drop-in (plan + execute) for every executor,
+with verify-as-it-lands: the per-block checksums the receivers compute WHILE
+the blocks stream in (lp_mc_verify) must equal the oracle's checksums of the
+CPU-generated source image, every epoch.  One GPU (nodes emulated on it)."""
+import pytest
+
+from paper_2502_09922_b200 import engine as E
+from paper_2502_09922_b200 import scaleout as SO
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def want():
+    from oracle import dataplane as D
+    cache = {}
+
+    def get(plan):
+        lay = plan.layout
+        key = (lay.weights_bytes, tuple(lay.block_lengths))
+        if key not in cache:
+            img = D.fill_image(lay, 0)
+            cache[key] = D.block_checksums(img, lay.block_offsets, lay.block_lengths)
+        return cache[key]
+    return get
+
+
+@pytest.mark.parametrize("n,k,b,host,executor,tile", [
+    (2, 1, 4, True, "hybrid", 1 << 20),
+    (3, 1, 4, True, "hybrid", 512 * 1024),
+    (5, 1, 4, True, "hybrid", 1 << 20),
+    (5, 2, 4, True, "hybrid", 1 << 20),
+    (4, 1, 4, False, "kernel", 1 << 20),
+    (4, 1, 4, False, "ce", 2 << 20),
+    (3, 1, 4, True, "kernel", 1 << 20),
+    (3, 1, 4, True, "ce", 1 << 20),
+    (4, 2, 3, False, "kernel", 4096 * 16),
+])
+def test_scale_out_verifies_while_landing(n, k, b, host, executor, tile, want):
+    plan = SO.plan_scale_out("tiny", n, k=k, block_count=b, host_source=host)
+    so = SO.ScaleOut(plan, executor=executor, tile_bytes=tile, pull_ctas=8, push_ctas=0,
+                     direction=1, copy_mode=0, verify=True, verify_ctas=8)
+    try:
+        so.load_sources()
+        ref = want(plan)
+        for _ in range(3):
+            for node in plan.receivers:   # wipe receivers so stale bytes cannot pass
+                E.N.call("lp_memset", E.C.c_void_p(so.cluster.node(node).image), 0,
+                         plan.layout.weights_bytes, None)
+            r = so.run()
+            gpu_receivers = [x for x in plan.receivers if so.cluster.node(x).kind == E.LP_NODE_GPU]
+            assert sorted(r.checksums) == gpu_receivers
+            for node in gpu_receivers:
+                assert r.checksums[node] == ref, (node, r.epoch)
+                assert so.checksums(node) == ref
+            assert r.launches == len(gpu_receivers) + (0 if executor == "ce" else so.kernel_launches)
+    finally:
+        so.close()
+
+
+def test_hybrid_is_the_host_policy():
+    plan = SO.plan_scale_out("tiny", 3, k=1, block_count=4, host_source=True)
+    assert SO.choose_executor(plan)[0] == "hybrid"
+    plan = SO.plan_scale_out("tiny", 4, k=1, block_count=4)
+    assert SO.choose_executor(plan)[0] == "ce"
