@@ -397,8 +397,8 @@ struct VerifyParams {
   int n_order;
 };
 
-__global__ void __launch_bounds__(256) verify_kernel(const VerifyParams p) {
-  __shared__ uint64_t part[8];
+__global__ void __launch_bounds__(512) verify_kernel(const VerifyParams p) {
+  __shared__ uint64_t part[16];
   __shared__ int s_ok;
   const uint64_t t0 = lp::globaltimer();
   if (threadIdx.x == 0) s_ok = 1;
@@ -427,12 +427,13 @@ __global__ void __launch_bounds__(256) verify_kernel(const VerifyParams p) {
         const uint64_t k0 = (uint64_t)(lo >> 3);
         const int T = blockDim.x;
         int64_t i = threadIdx.x;
-        for (; i + 3 * T < n16; i += 4 * T) {   // 64 B in flight per thread
-          ulonglong2 v[4];
+        constexpr int U = 8;
+        for (; i + (U - 1) * T < n16; i += U * T) {   // 128 B in flight per thread
+          ulonglong2 v[U];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) v[u] = __ldcs(w + i + u * T);
+          for (int u = 0; u < U; ++u) v[u] = __ldcs(w + i + u * T);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < U; ++u) {
             const uint64_t k = k0 + 2 * (uint64_t)(i + u * T);
             acc += lp::mix64(v[u].x ^ (k * G)) + lp::mix64(v[u].y ^ ((k + 1) * G));
           }
@@ -929,7 +930,7 @@ int lp_mc_verify(lp_mc* mc, int node, uint32_t epoch, int ctas, uint64_t* sums_d
   p.timeout_ns = mc->timeout_ns;
   p.epoch = epoch;
   p.n_order = nb;
-  verify_kernel<<<ctas, 256, 0, (cudaStream_t)stream>>>(p);
+  verify_kernel<<<ctas, 512, 0, (cudaStream_t)stream>>>(p);
   LP_CUDA(cudaGetLastError());
   return 0;
 }

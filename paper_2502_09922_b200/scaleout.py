@@ -127,7 +127,7 @@ class ScaleOut:
     def __init__(self, plan: ScaleOutPlan, distributed: bool = False, tile_bytes: int = E.DEFAULT_TILE,
                  push_ctas: int = 0, pull_ctas: int = 64, seed: int = 0, device: int = 0, direction: int = 1,
                  copy_mode: int = 1, chunk_bytes: int = 16384, executor: str = "kernel", ce_streams: int = 1,
-                 verify: bool = False, verify_ctas: int = 32):
+                 verify: bool = False, verify_ctas: int = 48):
         self.plan = plan
         self.distributed = distributed
         self.push_ctas, self.pull_ctas = push_ctas, pull_ctas
