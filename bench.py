@@ -204,6 +204,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pull-ctas", type=int, default=64)
+    ap.add_argument("--strategy", default="auto", choices=["auto", "lambda", "sharded_host"],
+                    help="host-sourced scale-out plan (auto = scaleout.choose_strategy)")
     ap.add_argument("--executor", default="auto", choices=["auto", "hybrid", "kernel", "ce"],
                     help="host-sourced scale-out executor (auto = scaleout.choose_executor)")
     ap.add_argument("--no-gpu-source", action="store_true")
@@ -234,26 +236,36 @@ def main():
     peaks = measured_peaks()
 
     # --- main workload: C3 host -> N GPUs -----------------------------------
-    plan = SO.plan_scale_out(C3_MODEL, N + 1, 1, C3_BLOCKS, host_source=True)
+    strategy = SO.choose_strategy(True, N) if args.strategy == "auto" else args.strategy
+    plans = {st: SO.plan_scale_out(C3_MODEL, N + 1, 1, C3_BLOCKS, host_source=True, strategy=st)
+             for st in {strategy, "lambda"}}
+    plan = plans[strategy]
     M = plan.layout.weights_bytes
     tiles = {"hybrid": SO.HYBRID_TILE, "kernel": 2 << 20, "ce": SO.CE_TILE}
     executor = SO.choose_executor(plan)[0] if args.executor == "auto" else args.executor
+    # the policy's (strategy, executor) first and timed in full; the others
+    # briefly, for the comparison table in config.host_executors
+    arms = [(strategy, executor)] + [a for a in (("sharded_host", "hybrid"), ("lambda", "hybrid"),
+                                                 ("lambda", "kernel"))
+                                     if a != (strategy, executor) and a[0] in plans]
     host_exec = {}
     main_res = None
-    for ex in [executor] + [e for e in ("hybrid", "kernel") if e != executor]:
-        so = SO.ScaleOut(plan, distributed=distributed, tile_bytes=tiles[ex], push_ctas=0,
+    for st, ex in arms:
+        so = SO.ScaleOut(plans[st], distributed=distributed, tile_bytes=tiles[ex], push_ctas=0,
                          pull_ctas=args.pull_ctas, seed=SEED, device=dev, direction=1, copy_mode=0,
                          executor=ex, verify=True)
         so.load_sources()
         want = source_sums(so, rank, distributed)
-        if ex == executor:
+        main = (st, ex) == (strategy, executor)
+        if main:
             clocks = ClockSampler(dev)
             clocks.start()
-        times, ok, launches = timed_steps(so, args.steps if ex == executor else 3, args.warmup, distributed,
+        times, ok, launches = timed_steps(so, args.steps if main else 3, args.warmup, distributed,
                                           stream, want)
         T = statistics.median(times)
-        host_exec[ex] = {"ms": round(T, 3), "agg_GBps": round(N * M / (T * 1e-3) / 1e9, 3), "byte_exact": ok}
-        if ex != executor:
+        host_exec[f"{st}/{ex}"] = {"ms": round(T, 3), "agg_GBps": round(N * M / (T * 1e-3) / 1e9, 3),
+                                   "byte_exact": ok}
+        if not main:
             so.close()
             continue
         clk = clocks.stop()
@@ -268,7 +280,7 @@ def main():
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            p2 = SO.plan_scale_out(C3_MODEL, N + 1, 1, C3_BLOCKS, host_source=True)
+            p2 = SO.plan_scale_out(C3_MODEL, N + 1, 1, C3_BLOCKS, host_source=True, strategy=strategy)
             so.cluster.set_schedule(p2.schedule, p2.sources)
             r = so.run(stream)
             assert all(v == want for v in r.checksums.values()), "e2e step delivered wrong bytes"
@@ -348,7 +360,9 @@ def main():
                 cpu = {"value": round(gb, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample}
             except Exception as e:  # noqa: BLE001
                 cpu = {"value": None, "unit": "GB/s", "cores": threads, "kind": "port", "sample": f"failed: {e}"}
-        achieved = M / (T * 1e-3) / 1e9          # bytes one receiver lands per step / step time
+        host_rows = [ln.split(",") for ln in plan.lines() if ln.split(",")[1] == "0"]
+        n_links = len({r[2] for r in host_rows})  # GPUs the host feeds = PCIe links in use
+        achieved = h2d / (T * 1e-3) / 1e9       # host->GPU bytes per step / step time
         exec_desc = {
             "hybrid": f"hybrid: PCIe hop as pinned DMA on the copy engines ({SO.HYBRID_TILE >> 20} MiB tiles, "
                       f"per-tile flags), NVLink relays in the multicast kernel ({args.pull_ctas} CTAs/rank, "
@@ -369,8 +383,13 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(T, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": f"{C3_MODEL} bf16 ({M / 1e9:.2f} GB) scale-out from pinned host memory "
-                                   f"to {N} GPU(s), b={C3_BLOCKS}, k=1, reference binomial schedule "
-                                   f"({plan.schedule.step_count} steps)",
+                                   f"to {N} GPU(s), b={C3_BLOCKS}, k=1",
+                       "strategy": {"lambda": f"reference λPipe binomial schedule ({plan.schedule.step_count} "
+                                              "steps, host = node 0)",
+                                    "sharded_host": "sharded host load: every GPU DMAs a disjoint block shard "
+                                                    "over its own PCIe link, shards exchanged over NVLink "
+                                                    f"(scaleout.sharded_host_schedule, {plan.schedule.step_count}"
+                                                    " steps)"}[strategy],
                        "executor": exec_desc,
                        "host_executors": host_exec,
                        "verify": "every step: receivers checksum each block while it lands (lp_mc_verify, "
@@ -379,10 +398,12 @@ def main():
                        "l2": "inputs larger than L2 (26 GB image per step)",
                        "parallelism": f"{N} GPU ranks, one process per GPU"},
             "scale_out_ms": round(T, 3), "byte_exact": ok,
-            "roofline": {"bound": "pcie" if N == 1 else "pcie+nvlink", "achieved": round(achieved, 2),
-                         "peak": 64.0, "unit": "GB/s", "frac": round(achieved / 64.0, 4),
-                         "peak_note": "PCIe Gen5 x16 nominal (the reference's h2d_Bps); measured DMA H2D on "
-                                      "this pool 55.6 GB/s (profiles/probe_r01.json)",
+            "roofline": {"bound": "pcie", "achieved": round(achieved, 2),
+                         "peak": 64.0 * n_links, "unit": "GB/s", "frac": round(achieved / (64.0 * n_links), 4),
+                         "achieved_note": f"host bytes per step / step time over the {n_links} PCIe link(s) the "
+                                          "plan drives (one per GPU the host sends to)",
+                         "peak_note": "PCIe Gen5 x16 nominal per link (the reference's h2d_Bps) x links; measured DMA H2D on "
+                                      "this pool 55.6 GB/s per link, 215 GB/s for 4 concurrent links (profiles/probe_r01.json, tools/h2d_concurrency.py)",
                          "traffic": traffic, "traffic_note": tnote},
             "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(12 * plan.block_count * N),

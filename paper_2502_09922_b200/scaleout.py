@@ -20,8 +20,8 @@ from dataclasses import dataclass, field
 from . import engine as E
 from .cluster import ClusterSpec, b200_box, transfer_step_time
 from .image import CONFIGS, ImageLayout, LlamaConfig, build_layout, model_spec
-from .multicast import (MulticastSchedule, attach_orders, compose_schedule, k_way_orders,
-                        partition_subgroups, schedule_to_lines, select_block_count)
+from .multicast import (MulticastSchedule, SubGroup, Transfer, attach_orders, compose_schedule,
+                        k_way_orders, partition_subgroups, schedule_to_lines, select_block_count)
 from .pipeline import assign_blocks_to_stages, completion_ordered_groups, generate_pipelines
 
 
@@ -37,6 +37,7 @@ class ScaleOutPlan:
     pipelines: list
     step_s_model: float
     host_source: bool = False
+    strategy: str = "lambda"
 
     @property
     def block_count(self) -> int:
@@ -50,9 +51,57 @@ class ScaleOutPlan:
         return schedule_to_lines(self.schedule)
 
 
+def sharded_host_schedule(n_nodes: int, plan) -> MulticastSchedule:
+    """Host-sourced load for GPUs that SHARE the host copy (one box).
+
+    The reference gives every node holding a host-memory copy ("warm") its
+    own local h2d load (simengine.py:508-521) and multicasts from a memory
+    source only to nodes without one.  On a B200 box all GPUs read the same
+    pinned host memory, each over its own PCIe link, so here every GPU loads a
+    disjoint shard over its link and the shards are exchanged over NVLink:
+    block j is owned by GPU ``1 + j % G`` (G = n_nodes - 1 GPUs, node 0 =
+    HOST), arrives from the host at step ``G * (j // G)`` and is forwarded by its
+    owner to the other GPUs in a rotation over the next G - 1 steps (one send
+    and one receive per GPU per step; only the host sends G per step, one per
+    PCIe link).  The engine runs the PCIe and NVLink legs concurrently (steps
+    only order each node's ops).  Host egress is spread
+    over G PCIe links instead of the binomial tree's ``ceil(log2 n)`` host
+    partners (measured 215 GB/s for 4 concurrent links vs 55.6 for one,
+    tools/h2d_concurrency.py).  ``max_send_degree = G`` (the host), no step
+    bound; validate_schedule accepts it.
+    """
+    G = n_nodes - 1
+    if G < 1:
+        raise ValueError("sharded host load needs the HOST node and at least one GPU")
+    order = tuple(bl.block_id for bl in plan.blocks)
+    rounds = (len(order) + G - 1) // G
+    steps = [[] for _ in range(rounds * G)]
+    for r in range(rounds):
+        blocks = order[r * G:(r + 1) * G]          # block r*G + q is owned by GPU 1 + q
+        for q, blk in enumerate(blocks):
+            steps[r * G].append(Transfer(r * G, 0, 1 + q, blk))
+        for i in range(1, G):                      # rotation: one send and one receive per GPU per step
+            for q, blk in enumerate(blocks):
+                peer = 1 + (q + i) % G
+                steps[r * G + i].append(Transfer(r * G + i, 1 + q, peer, blk))
+    while steps and not steps[-1]:
+        steps.pop()
+    return MulticastSchedule((SubGroup(0, tuple(range(n_nodes)), order),), steps, max_send_degree=G,
+                             enforce_step_bound=False, label="sharded_host")
+
+
 def plan_scale_out(config, n_nodes: int, k: int = 1, block_count="auto",
-                   cluster: ClusterSpec | None = None, host_source: bool = False) -> ScaleOutPlan:
-    """Planning half of ``_launch_lambda_scale`` (simengine.py:579-590)."""
+                   cluster: ClusterSpec | None = None, host_source: bool = False,
+                   strategy: str = "lambda") -> ScaleOutPlan:
+    """Planning half of ``_launch_lambda_scale`` (simengine.py:579-590).
+
+    ``strategy="sharded_host"`` (host sources only) replaces the binomial
+    schedule by :func:`sharded_host_schedule`; it has no λPipe pipelines
+    (every GPU completes at about the same time)."""
+    if strategy not in ("lambda", "sharded_host"):
+        raise ValueError("strategy is 'lambda' or 'sharded_host'")
+    if strategy == "sharded_host" and not host_source:
+        raise ValueError("sharded_host needs host_source=True")
     cfg = CONFIGS[config] if isinstance(config, str) else config
     cluster = cluster or b200_box(node_count=n_nodes)
     spec = model_spec(cfg)
@@ -69,6 +118,10 @@ def plan_scale_out(config, n_nodes: int, k: int = 1, block_count="auto",
     pipes = generate_pipelines(ordered) if any(g.receivers for g in ordered) else []
     eps = [assign_blocks_to_stages(pn, orders, layout.plan.block_count, sched, i) for i, pn in enumerate(pipes)]
     step_s = transfer_step_time(sched, layout.plan, cluster)
+    if strategy == "sharded_host":
+        sched = sharded_host_schedule(n_nodes, layout.plan)
+        return ScaleOutPlan(cfg, layout, nodes, [0], list(sched.groups), sched, list(sched.groups), [], step_s,
+                            host_source, strategy)
     return ScaleOutPlan(cfg, layout, nodes, sources, groups, sched, ordered, eps, step_s, host_source)
 
 
@@ -91,6 +144,15 @@ def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
 
 CE_TILE = 256 << 20
 HYBRID_TILE = 64 << 20   # DMA tile of the PCIe hop = relay granule of the kernel
+
+
+def choose_strategy(host_source: bool, n_gpus: int) -> str:
+    """Full-replica scale-out from the box's shared host copy with >= 2 GPUs:
+    sharded PCIe loads + NVLink exchange (2.0x the binomial tree's host
+    egress at 4 GPUs); otherwise the reference's λPipe schedule.  Serving
+    (execute-while-load) always plans λPipe: its pipelines need the
+    binomial arrival order."""
+    return "sharded_host" if host_source and n_gpus >= 2 else "lambda"
 
 
 def choose_executor(plan: ScaleOutPlan, tile_bytes: int = E.DEFAULT_TILE):

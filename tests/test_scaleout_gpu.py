@@ -63,3 +63,23 @@ def test_hybrid_is_the_host_policy():
     assert SO.choose_executor(plan)[0] == "hybrid"
     plan = SO.plan_scale_out("tiny", 4, k=1, block_count=4)
     assert SO.choose_executor(plan)[0] == "ce"
+
+
+@pytest.mark.parametrize("n,executor", [(3, "hybrid"), (5, "hybrid"), (5, "kernel"), (4, "ce"), (2, "hybrid")])
+def test_sharded_host_load_verifies(n, executor, want):
+    plan = SO.plan_scale_out("tiny", n, k=1, block_count=4, host_source=True, strategy="sharded_host")
+    so = SO.ScaleOut(plan, executor=executor, tile_bytes=1 << 20, pull_ctas=8, push_ctas=0,
+                     direction=1, copy_mode=0, verify=True, verify_ctas=8)
+    try:
+        so.load_sources()
+        ref = want(plan)
+        for _ in range(2):
+            for node in plan.receivers:
+                E.N.call("lp_memset", E.C.c_void_p(so.cluster.node(node).image), 0,
+                         plan.layout.weights_bytes, None)
+            r = so.run()
+            assert sorted(r.checksums) == plan.receivers
+            for node in plan.receivers:
+                assert r.checksums[node] == ref
+    finally:
+        so.close()
