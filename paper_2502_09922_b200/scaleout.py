@@ -189,7 +189,7 @@ class ScaleOut:
     def __init__(self, plan: ScaleOutPlan, distributed: bool = False, tile_bytes: int = E.DEFAULT_TILE,
                  push_ctas: int = 0, pull_ctas: int = 64, seed: int = 0, device: int = 0, direction: int = 1,
                  copy_mode: int = 1, chunk_bytes: int = 16384, executor: str = "kernel", ce_streams: int = 1,
-                 verify: bool = False, verify_ctas: int = 48):
+                 verify: bool = False, verify_ctas: int | None = None):
         self.plan = plan
         self.distributed = distributed
         self.push_ctas, self.pull_ctas = push_ctas, pull_ctas
@@ -213,7 +213,11 @@ class ScaleOut:
         self.kernel_launches = 0      # multicast kernels of the last run (this process)
         # verify-as-it-lands (lp_mc_verify): receivers checksum every block
         # while it streams in; run() returns the sums (a d2h of 8 B per block)
-        self.verify, self.verify_ctas = verify, verify_ctas
+        # 48 CTAs checksum ~880 GB/s (profiles/verify_kernel_full_r01.csv),
+        # enough beside the SM executors; the copy-engine executor leaves every
+        # SM free, so NVLink-rate landings get 96
+        self.verify = verify
+        self.verify_ctas = verify_ctas or (96 if executor == "ce" else 48)
         self._vbuf = {}
         self.seed = seed
         self.device = device
