@@ -280,9 +280,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmW2,
                            const __grid_constant__ CUtensorMap tmX, const GemmArgs args) {
   using C = Cfg<BT, EPI>;
-  static_assert(2 * C::ACC_COLS <= 512, "two accumulators must fit TMEM");
-  constexpr int TCOLS = 2 * C::ACC_COLS <= 32 ? 32 : 2 * C::ACC_COLS <= 64 ? 64 : 2 * C::ACC_COLS <= 128 ? 128
-                        : 2 * C::ACC_COLS <= 256 ? 256 : 512;
+  // two TMEM accumulator buffers (epilogue of tile i overlaps the MMAs of
+  // tile i+1) when they fit the 512 columns; SwiGLU at BT = 256 holds gate and
+  // up accumulators of 256 columns each, so it runs single-buffered — still
+  // faster than BT = 128, whose 128x128x16 MMAs need 128 B/clk of smem operand
+  // reads (the SM's whole smem bandwidth) against 96 B/clk at N = 256
+  constexpr int NBUF = 2 * C::ACC_COLS <= 512 ? 2 : 1;
+  constexpr int TC = NBUF * C::ACC_COLS;
+  constexpr int TCOLS = TC <= 32 ? 32 : TC <= 64 ? 64 : TC <= 128 ? 128 : TC <= 256 ? 256 : 512;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[C::STAGES];
   __shared__ __align__(8) uint64_t empty_bar[C::STAGES];
@@ -358,8 +363,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++li) {
       int n0, t0, kb0, nkb;
       tile_coords(tile, n0, t0, kb0, nkb);
-      const int a = li & 1;
-      lp::mbar_wait(&tempty[a], ((li >> 1) & 1) ^ 1);    // epilogue drained this accumulator
+      const int a = li % NBUF;
+      lp::mbar_wait(&tempty[a], ((li / NBUF) & 1) ^ 1);  // epilogue drained this accumulator
       tc_fence_after();
       const uint32_t acc_base = tmem + a * C::ACC_COLS;
       for (int i = 0; i < nkb; ++i, ++it) {
@@ -388,8 +393,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++li) {
       int n0, t0, kb0, nkb;
       tile_coords(tile, n0, t0, kb0, nkb);
-      const int a = li & 1;
-      lp::mbar_wait(&tfull[a], (li >> 1) & 1);
+      const int a = li % NBUF;
+      lp::mbar_wait(&tfull[a], (li / NBUF) & 1);
       tc_fence_after();
       const int n = n0 + row;
       constexpr int CH = BT < 32 ? BT : 32;
@@ -526,12 +531,8 @@ int dispatch(const void* W, const void* W2, int64_t N, int64_t K, const void* X,
   if (T <= 16) return launch<16, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
   if (T <= 32) return launch<32, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
   if (T <= 64) return launch<64, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
-  if constexpr (EPI == EPI_SWIGLU) {
-    return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
-  } else {
-    if (T <= 128) return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
-    return launch<256, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
-  }
+  if (T <= 128) return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  return launch<256, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
 }
 
 }  // namespace

@@ -96,14 +96,37 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, int H, int KV, int
 // keys, every lane computes its key's G dot products from 16-byte K loads
 // against q in smem (no per-key shuffles), one max/sum reduction per chunk,
 // then P.V with the chunk's probabilities broadcast lane by lane while each
-// lane accumulates its hd/32 output dims.  Warps merge through smem.
+// lane accumulates its HD/32 output dims.  Warps merge through smem.
+// HD is a template parameter so both phases issue their loads in batches
+// (all HD/8 K vectors of a key, then V rows 8 keys at a time) before using
+// them: a decode CTA is latency bound, and a load -> FMA chain per key was
+// 45 us per layer at B = 16 (profiles/decode_step_launches_r01.csv).
 constexpr int ATT_WARPS = 4;
 constexpr int MAX_G = 8;
-constexpr int MAX_HD = 128;
+constexpr int PV_BATCH = 8;
+
+template <int PER>
+__device__ __forceinline__ void load_v(const __nv_bfloat16* p, float (&f)[4]) {
+  if constexpr (PER == 4) {
+    const uint2 raw = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+  } else if constexpr (PER == 2) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+    f[0] = a.x; f[1] = a.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) f[i] = __bfloat162float(p[i]);
+  }
+}
+
+template <int HD>
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
-    int H, int KV, int hd, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
+    int H, int KV, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
+  constexpr int PER = HD / 32;   // output dims per lane
   lp::pdl_wait();
   lp::pdl_trigger();
   const int t = blockIdx.x;
@@ -111,22 +134,21 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
   const int G = H / KV;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = pos[t] + 1;
-  const int per = hd / 32;  // output dims per lane (<= 4)
-  const __nv_bfloat16* kb = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * hd;
-  const __nv_bfloat16* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * hd;
-  __shared__ float sq[MAX_G][MAX_HD];
-  for (int i = threadIdx.x; i < G * hd; i += blockDim.x) {
-    const int g = i / hd, dd = i % hd;
-    sq[g][dd] = __bfloat162float(q[((int64_t)t * H + kh * G + g) * hd + dd]) * scale;
+  const __nv_bfloat16* kb = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+  const __nv_bfloat16* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+  __shared__ float sq[MAX_G][HD];
+  for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
+    const int g = i / HD, dd = i % HD;
+    sq[g][dd] = __bfloat162float(q[((int64_t)t * H + kh * G + g) * HD + dd]) * scale;
   }
   __syncthreads();
-  float m[MAX_G], l[MAX_G], acc[MAX_G][4];
+  float m[MAX_G], l[MAX_G], acc[MAX_G][PER];
 #pragma unroll
   for (int g = 0; g < MAX_G; ++g) {
     m[g] = -INFINITY;
     l[g] = 0.f;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[g][i] = 0.f;
+    for (int i = 0; i < PER; ++i) acc[g][i] = 0.f;
   }
   for (int c0 = warp * 32; c0 < L; c0 += ATT_WARPS * 32) {
     const int j = c0 + lane;
@@ -135,10 +157,13 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
 #pragma unroll
     for (int g = 0; g < MAX_G; ++g) s[g] = 0.f;
     if (live) {
-      const int4* kr = reinterpret_cast<const int4*>(kb + (int64_t)j * hd);
-      for (int v8 = 0; v8 < hd / 8; ++v8) {
-        const int4 raw = kr[v8];
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const int4* kr = reinterpret_cast<const int4*>(kb + (int64_t)j * HD);
+      int4 raw[HD / 8];
+#pragma unroll
+      for (int v8 = 0; v8 < HD / 8; ++v8) raw[v8] = kr[v8];
+#pragma unroll
+      for (int v8 = 0; v8 < HD / 8; ++v8) {
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[v8]);
         float kf[8];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -158,50 +183,53 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
     float p[MAX_G];
 #pragma unroll
     for (int g = 0; g < MAX_G; ++g) {
-      if (g >= G) break;
+      p[g] = 0.f;
+      if (g >= G) continue;
       const float cm = warp_max(live ? s[g] : -INFINITY);
       const float mn = fmaxf(m[g], cm);
       const float corr = __expf(m[g] - mn);
       p[g] = live ? __expf(s[g] - mn) : 0.f;
       l[g] = l[g] * corr + warp_sum(p[g]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[g][i] *= corr;
+      for (int i = 0; i < PER; ++i) acc[g][i] *= corr;
       m[g] = mn;
     }
     const int nk = min(32, L - c0);
-    for (int jj = 0; jj < nk; ++jj) {
-      const __nv_bfloat16* vr = vb + (int64_t)(c0 + jj) * hd + lane * per;
-      float vf[4];
-      if (per == 4) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(vr);
-        const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-        const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-        vf[0] = f0.x; vf[1] = f0.y; vf[2] = f1.x; vf[3] = f1.y;
-      } else {
-        for (int i = 0; i < per; ++i) vf[i] = __bfloat162float(vr[i]);
+    for (int j0 = 0; j0 < nk; j0 += PV_BATCH) {
+      float vf[PV_BATCH][4];
+#pragma unroll
+      for (int b = 0; b < PV_BATCH; ++b) {
+        const int key = c0 + min(j0 + b, nk - 1);     // clamped: dead keys have p = 0
+        load_v<PER>(vb + (int64_t)key * HD + lane * PER, vf[b]);
       }
 #pragma unroll
-      for (int g = 0; g < MAX_G; ++g) {
-        if (g >= G) break;
-        const float pj = __shfl_sync(0xffffffffu, p[g], jj);
+      for (int b = 0; b < PV_BATCH; ++b) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i < per) acc[g][i] += pj * vf[i];
+        for (int g = 0; g < MAX_G; ++g) {
+          if (g >= G) break;
+          const float pj = __shfl_sync(0xffffffffu, p[g], (j0 + b) & 31);
+          const float w = (j0 + b < nk) ? pj : 0.f;
+#pragma unroll
+          for (int i = 0; i < PER; ++i) acc[g][i] += w * vf[b][i];
+        }
       }
     }
   }
   __shared__ float sm_m[ATT_WARPS][MAX_G], sm_l[ATT_WARPS][MAX_G];
-  __shared__ float sm_acc[ATT_WARPS][MAX_G][MAX_HD];
-  for (int g = 0; g < G; ++g) {
+  __shared__ float sm_acc[ATT_WARPS][MAX_G][HD];
+#pragma unroll
+  for (int g = 0; g < MAX_G; ++g) {
+    if (g >= G) break;
     if (lane == 0) {
       sm_m[warp][g] = m[g];
       sm_l[warp][g] = l[g];
     }
-    for (int i = 0; i < per; ++i) sm_acc[warp][g][lane * per + i] = acc[g][i];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) sm_acc[warp][g][lane * PER + i] = acc[g][i];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < G * hd; idx += blockDim.x) {
-    const int g = idx / hd, dcol = idx % hd;
+  for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
+    const int g = idx / HD, dcol = idx % HD;
     float mx = -INFINITY;
     for (int w = 0; w < ATT_WARPS; ++w) mx = fmaxf(mx, sm_m[w][g]);
     float den = 0.f, num = 0.f;
@@ -211,7 +239,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
       den += sm_l[w][g] * f;
       num += sm_acc[w][g][dcol] * f;
     }
-    out[((int64_t)t * H + kh * G + g) * hd + dcol] = __float2bfloat16_rn(num / den);
+    out[((int64_t)t * H + kh * G + g) * HD + dcol] = __float2bfloat16_rn(num / den);
   }
 }
 
@@ -340,9 +368,17 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
   LP_CHECK(n_kv > 0 && n_heads % n_kv == 0 && n_heads / n_kv <= MAX_G, "lp_attention: GQA group > %d", MAX_G);
   LP_CHECK(head_dim % 32 == 0 && head_dim <= 128, "lp_attention: head_dim must be 32..128, multiple of 32");
   dim3 grid((unsigned)T, (unsigned)n_kv);
-  LP_CUDA(lp::launch(attention_kernel, grid, dim3(ATT_WARPS * 32), 0, (cudaStream_t)stream,
-                     (const __nv_bfloat16*)q, (const __nv_bfloat16*)k_cache, (const __nv_bfloat16*)v_cache, pos, seq,
-                     n_heads, n_kv, head_dim, max_len, scale, (__nv_bfloat16*)out));
+  const __nv_bfloat16 *qq = (const __nv_bfloat16*)q, *kk = (const __nv_bfloat16*)k_cache,
+                      *vv = (const __nv_bfloat16*)v_cache;
+  __nv_bfloat16* oo = (__nv_bfloat16*)out;
+  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 blk(ATT_WARPS * 32);
+  switch (head_dim) {
+    case 32: LP_CUDA(lp::launch(attention_kernel<32>, grid, blk, 0, s, qq, kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)); break;
+    case 64: LP_CUDA(lp::launch(attention_kernel<64>, grid, blk, 0, s, qq, kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)); break;
+    case 96: LP_CUDA(lp::launch(attention_kernel<96>, grid, blk, 0, s, qq, kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)); break;
+    default: LP_CUDA(lp::launch(attention_kernel<128>, grid, blk, 0, s, qq, kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)); break;
+  }
   return 0;
 }
 

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import time
 
 from . import _native as N
 from .engine import device_view
@@ -43,6 +44,17 @@ def _cur_stream(stream):
         return stream
     import torch
     return torch.cuda.current_stream().cuda_stream
+
+
+def _upload(graph):
+    """Replay a freshly captured graph once (its static inputs still point
+    every row at the scratch sequence slot, so nothing live is touched): the
+    first launch of an instantiated graph uploads it to the device, which
+    measured 30+ ms for a 32-layer prefill graph — paid here, before the
+    serving clock, instead of by the first request after the mode switch."""
+    import torch
+    graph.replay()
+    torch.cuda.current_stream().synchronize()
 
 
 class KVCache:
@@ -219,6 +231,7 @@ class DecodeGraph:
                     self.out = self._body()
             finally:
                 N.lib().lp_set_pdl(0)
+            _upload(self.graph)
 
     def step(self, tokens, pos, seq):
         """Decode one token for each live row; returns the int32 device tensor."""
@@ -283,6 +296,7 @@ class PrefillGraph:
                     self.out = self._body()
             finally:
                 N.lib().lp_set_pdl(0)
+            _upload(self.graph)
 
     def step(self, tokens, pos, seq, last):
         """Prefill; returns the next token of each request (pinned host tensor,
@@ -294,6 +308,7 @@ class PrefillGraph:
             raise ValueError("prefill larger than the captured graph")
         if self.graph is None:
             self.capture()
+        t0 = time.perf_counter()
         buf = self.h_in.numpy()
         buf[:n] = tokens
         buf[n:c] = 0
@@ -304,9 +319,13 @@ class PrefillGraph:
         buf[3 * c:3 * c + m] = last
         buf[3 * c + m:] = 0
         with torch.cuda.device(self.ex.device):
+            t1 = time.perf_counter()
             self.d_in.copy_(self.h_in, non_blocking=True)
+            t2 = time.perf_counter()
             self.graph.replay()
+            t3 = time.perf_counter()
             self.h_out.copy_(self.out, non_blocking=True)
+        self.last_timing = (t1 - t0, t2 - t1, t3 - t2, time.perf_counter() - t3)   # host s: fill, h2d, replay, d2h
         return self.h_out[:m]
 
 
@@ -367,6 +386,7 @@ class SegmentGraph:
                     self.tok = self._body()
             finally:
                 N.lib().lp_set_pdl(0)
+            _upload(self.graph)
 
     def stage_inputs(self, tokens, pos, seq, last):
         c = self.cap

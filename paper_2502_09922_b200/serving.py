@@ -29,6 +29,7 @@ timeline unchanged.
 
 from __future__ import annotations
 
+import os
 import time
 from collections import deque
 from dataclasses import dataclass, field
@@ -117,6 +118,7 @@ class Server:
         self.prefill_ms_per_token = prefill_ms_per_token
         self.events = []
         self.profile = []          # per iteration: (start, enqueue s, device s, tokens, unit batches)
+        self.profile_detail = [] if os.environ.get("LP_SERVE_PROFILE") else None
         self.units = {}
         self._next_uid = 0
         self.switched = False
@@ -248,7 +250,7 @@ class Server:
             self.log(now, "mode_switch", model=self.cfg.name, nodes=sorted(switched_nodes), mode="local")
         self.switched = True
 
-    PREFILL_BUCKETS = (128, 256, 512, 1024, 2048)
+    PREFILL_BUCKETS = (128, 256, 384, 512, 768, 1024, 1536, 2048)
 
     def _prefill_graph(self, u, n_tokens):
         """Smallest captured prefill graph that fits (captured on demand)."""
@@ -309,8 +311,13 @@ class Server:
                         pos += list(range(len(ctx)))
                         seq += [r.slot] * len(ctx)
                         last.append(len(tokens) - 1)
+                    t_pf = time.perf_counter()
                     with self.torch.cuda.device(u.stages[0].device):
                         out.append((reqs, pf.step(tokens, pos, seq, last)))
+                    if self.profile_detail is not None:
+                        self.profile_detail.append(("prefill_enqueue", u.uid, pf.cap, time.perf_counter() - t_pf))
+                        self.profile_detail.append(("prefill_parts " + " ".join("%.4f" % v for v in pf.last_timing),
+                                                    u.uid, pf.cap, 0.0))
                     reqs = []
             if not reqs:
                 return out
@@ -395,7 +402,10 @@ class Server:
                 queue.append(r)
                 self.log(rec.arrival_s, "request_arrival", request=rec.request_id, model=rec.model_id)
             if not self.switched:
+                t_cn = time.perf_counter()
                 done = self.cluster.complete_nodes(epoch)
+                if self.profile_detail is not None:
+                    self.profile_detail.append(("complete_nodes", -1, 0, time.perf_counter() - t_cn))
                 now = time.perf_counter() - self.t0
                 for n in self.receivers:
                     if n not in self.block_complete_s and all(done[n]):
@@ -408,7 +418,10 @@ class Server:
                             self.activation_s[u.uid] = now
                 all_done = all(all(done[n]) for n in self.receivers)
                 if all_done and tokens_emitted >= self.switch_hold_tokens:
+                    t_ms = time.perf_counter()
                     self._mode_switch(now)
+                    if self.profile_detail is not None:
+                        self.profile_detail.append(("mode_switch", -1, 0, time.perf_counter() - t_ms))
             self._admit(queue)
             t_enq = time.perf_counter()
             work = []

@@ -43,7 +43,8 @@ def test_gemm_matches_fp32(n, k, t, epi, split):
     assert (out - ref).abs().max().item() < tol
 
 
-@pytest.mark.parametrize("n,k,t", [(688, 256, 24), (1536, 512, 1), (640, 1024, 130)])
+@pytest.mark.parametrize("n,k,t", [(688, 256, 24), (1536, 512, 1), (640, 1024, 130), (1408, 512, 600),
+                                   (384, 4096, 257)])
 def test_gemm_swiglu_matches_fp32(n, k, t):
     import torch
     g = torch.Generator(device="cuda").manual_seed(n + k)
@@ -55,6 +56,37 @@ def test_gemm_swiglu_matches_fp32(n, k, t):
     N.check(N.lib().lp_gemm_swiglu(_ptr(wg), _ptr(wu), n, k, _ptr(x), t, _ptr(out), n, None))
     torch.cuda.synchronize()
     assert ((out.float() - ref).abs() / (ref.abs() + 0.1)).max().item() < 0.05
+
+
+@pytest.mark.parametrize("hd,H,KV,ctx", [(128, 32, 8, [1, 150, 37, 300]), (64, 4, 2, [5, 129, 64]),
+                                          (128, 64, 8, [200, 17]), (128, 8, 8, [33, 96])])
+def test_attention_matches_fp32(hd, H, KV, ctx):
+    """Ragged causal GQA attention (decode rows at arbitrary positions and a
+    prefill-style run of consecutive positions) vs a torch fp32 softmax."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(hd + H + len(ctx))
+    seqs, max_len = len(ctx), max(ctx) + 8
+    kc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
+    pos = [c - 1 for c in ctx] + list(range(ctx[0] - 1, max(ctx[0] - 40, -1), -1))
+    seq = list(range(seqs)) + [0] * (len(pos) - seqs)
+    T = len(pos)
+    q = torch.randn(T, H, hd, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(T, H, hd, dtype=torch.bfloat16, device="cuda")
+    p_t = torch.tensor(pos, dtype=torch.int32, device="cuda")
+    s_t = torch.tensor(seq, dtype=torch.int32, device="cuda")
+    scale = 1.0 / math.sqrt(hd)
+    N.check(N.lib().lp_attention(_ptr(q), _ptr(kc), _ptr(vc), _ptr(p_t), _ptr(s_t), T, H, KV, hd, max_len,
+                                 N.C.c_float(scale), _ptr(out), None))
+    torch.cuda.synchronize()
+    G = H // KV
+    for t in range(T):
+        L = pos[t] + 1
+        k = kc[seq[t], :, :L].float().repeat_interleave(G, 0)      # [H, L, hd]
+        v = vc[seq[t], :, :L].float().repeat_interleave(G, 0)
+        w = torch.softmax(torch.einsum("hd,hld->hl", q[t].float() * scale, k), -1)
+        ref = torch.einsum("hl,hld->hd", w, v)
+        assert (out[t].float() - ref).abs().max().item() < 2e-2, f"token {t} (pos {pos[t]})"
 
 
 @pytest.fixture(scope="module")

@@ -69,6 +69,8 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
                         u.graph.graph.replay()
                     torch.cuda.synchronize(d)
                     print(f"replay node {n} dev {d}: {(_t.perf_counter() - t0) / 5 * 1e3:.2f} ms", file=sys.stderr)
+            for row in srv2.profile_detail or []:
+                print("detail %s unit=%d cap=%d %.4f s" % row, file=sys.stderr)
             for row in srv2.profile:
                 print("iter t=%.4f enq=%.4f dev=%.4f tokens=%d batches=%d" % row, file=sys.stderr)
         return {
