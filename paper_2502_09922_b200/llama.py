@@ -46,6 +46,47 @@ def _cur_stream(stream):
     return torch.cuda.current_stream().cuda_stream
 
 
+SMS = 148
+
+
+def gemm_token_tile(tokens: int) -> int:
+    """Token tile lp_gemm_bf16 dispatches for ``tokens`` (lp_gemm.cu dispatch())."""
+    for bt in (16, 32, 64, 128):
+        if tokens <= bt:
+            return bt
+    return 256
+
+
+def gemm_split(n_rows: int, k: int, tokens: int) -> int:
+    """K splits for the accumulating (residual-add) GEMM.
+
+    Decode (T <= 64, one CTA per work item, 2 per SM): ~160 CTAs measured
+    best (profiles/gemm_split_sweep_r01.txt).  Prefill (persistent, one CTA
+    per SM): the split maximising wave efficiency (work items / 148-SM
+    slots), discounted 2 % per extra split — e.g. QKV at T = 256 has only 48 tiles of 128 x 256, so
+    48 of 148 SMs would work without a 3-way split.  Each split keeps >= 8
+    k-blocks of 64."""
+    tiles = -(-n_rows // 128) * -(-tokens // gemm_token_tile(tokens))
+    kb = -(-k // 64)
+    if tokens <= 64:
+        return max(1, min(round(160 / max(tiles, 1)), max(1, kb // 4)))
+    if tiles >= 2 * SMS:
+        # >= 2 waves: tiles finish at staggered times, so quantisation costs
+        # less than modelled, while shorter K per item exposes the red.add
+        # epilogue (T = 4096 QKV: 167 us unsplit vs 192 us at 3 splits)
+        return 1
+    best, best_score = 1, 0.0
+    for split in range(1, 9):
+        if split > 1 and kb // split < 8:
+            break
+        items = tiles * split
+        eff = items / (-(-items // SMS) * SMS)
+        score = eff * (1.0 - 0.02 * (split - 1))    # each split re-adds T x N partial sums
+        if score > best_score + 1e-9:
+            best, best_score = split, score
+    return best
+
+
 def _upload(graph):
     """Replay a freshly captured graph once (its static inputs still point
     every row at the scratch sequence slot, so nothing live is touched): the
@@ -100,10 +141,7 @@ class LlamaExecutor:
 
     # -- kernels ------------------------------------------------------------------
     def _gemm_add(self, w: int, n_rows: int, k: int, x, tokens: int, out, ldo: int, stream: int):
-        tiles = -(-n_rows // 128) * -(-tokens // 128)
-        # ~160 CTAs (just over one wave of 148 SMs) measured best for decode
-        # shapes (profiles/gemm_split_sweep_r01.txt); keep >= 4 k-blocks per split
-        split = max(1, min(round(160 / max(tiles, 1)), max(1, (k // 64) // 4)))
+        split = gemm_split(n_rows, k, tokens)
         N.check(self.lib.lp_gemm_bf16(C.c_void_p(w), n_rows, k, _vp(x), tokens, _vp(out), ldo, 0, split,
                                       C.c_void_p(stream)), "lp_gemm_bf16")
 

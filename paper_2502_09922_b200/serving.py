@@ -215,16 +215,21 @@ class Server:
 
     # -- scheduling --------------------------------------------------------------
     def _admit(self, queue):
-        for u in sorted(self.units.values(), key=lambda x: x.uid):
-            if not u.active or u.retired:
-                continue
-            while queue:
-                s = u.free_slot()
-                if s < 0:
-                    break
-                r = queue.popleft()
-                r.unit, r.slot, r.kv_len, r.needs_prefill = u.uid, s, 0, True
-                u.busy[s] = r
+        """FIFO admission (simengine.py:356-368).  Each request goes to the
+        active unit with the most free slots, ties to the lowest unit id: with
+        the reference's one slot per local unit (``batch_slots = 1``) that is
+        exactly its unit-order fill; with 16-slot continuous-batching replicas
+        it spreads a burst over the replicas instead of stacking every prefill
+        on the first one."""
+        live = [u for u in sorted(self.units.values(), key=lambda x: x.uid) if u.active and not u.retired]
+        while queue and live:
+            u = max(live, key=lambda x: (x.slots - len(x.busy), -x.uid))
+            s = u.free_slot()
+            if s < 0:
+                break
+            r = queue.popleft()
+            r.unit, r.slot, r.kv_len, r.needs_prefill = u.uid, s, 0, True
+            u.busy[s] = r
 
     def _mode_switch(self, now):
         switched_nodes = []
@@ -302,7 +307,19 @@ class Server:
                     tok = u.graph.step([r.out[-1] for r in dec], [r.kv_len for r in dec], [r.slot for r in dec])
                 out.append((dec, tok))
             if reqs:
-                pf = self._prefill_graph(u, sum(len(r.prompt) + len(r.out) for r in reqs))
+                # one graph replay per iteration: requests beyond the largest
+                # bucket keep needs_prefill and go in the next iteration
+                # (an eager 32-layer forward would cost ~50 ms of launches)
+                cap_max = max(c for c in self.PREFILL_BUCKETS if c <= self.max_len * u.slots)
+                take, n_tok = [], 0
+                for r in reqs:
+                    n = len(r.prompt) + len(r.out)
+                    if take and n_tok + n > cap_max:
+                        break
+                    take.append(r)
+                    n_tok += n
+                reqs = take
+                pf = self._prefill_graph(u, n_tok)
                 if pf is not None:
                     tokens, pos, seq, last = [], [], [], []
                     for r in reqs:
@@ -314,7 +331,7 @@ class Server:
                     t_pf = time.perf_counter()
                     with self.torch.cuda.device(u.stages[0].device):
                         out.append((reqs, pf.step(tokens, pos, seq, last)))
-                    if self.profile_detail is not None:
+                    if getattr(self, "profile_detail", None) is not None:
                         self.profile_detail.append(("prefill_enqueue", u.uid, pf.cap, time.perf_counter() - t_pf))
                         self.profile_detail.append(("prefill_parts " + " ".join("%.4f" % v for v in pf.last_timing),
                                                     u.uid, pf.cap, 0.0))
@@ -404,7 +421,7 @@ class Server:
             if not self.switched:
                 t_cn = time.perf_counter()
                 done = self.cluster.complete_nodes(epoch)
-                if self.profile_detail is not None:
+                if getattr(self, "profile_detail", None) is not None:
                     self.profile_detail.append(("complete_nodes", -1, 0, time.perf_counter() - t_cn))
                 now = time.perf_counter() - self.t0
                 for n in self.receivers:
@@ -420,7 +437,7 @@ class Server:
                 if all_done and tokens_emitted >= self.switch_hold_tokens:
                     t_ms = time.perf_counter()
                     self._mode_switch(now)
-                    if self.profile_detail is not None:
+                    if getattr(self, "profile_detail", None) is not None:
                         self.profile_detail.append(("mode_switch", -1, 0, time.perf_counter() - t_ms))
             self._admit(queue)
             t_enq = time.perf_counter()

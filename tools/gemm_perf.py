@@ -8,6 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2502_09922_b200 import _native as N  # noqa: E402
+from paper_2502_09922_b200.llama import gemm_split  # noqa: E402
 
 P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 lib = N.lib()
@@ -26,7 +27,11 @@ def timeit(fn, iters=20):
     return e0.elapsed_time(e1) / iters
 
 
-shapes = [("qkv", 6144, 4096), ("wo", 4096, 4096), ("gate_up", 14336, 4096), ("down", 4096, 14336)]
+SHAPES = {
+    "llama3-8b": [("qkv", 6144, 4096), ("wo", 4096, 4096), ("gate_up", 14336, 4096), ("down", 4096, 14336)],
+    "llama3-70b": [("qkv", 10240, 8192), ("wo", 8192, 8192), ("gate_up", 28672, 8192), ("down", 8192, 28672)],
+}
+shapes = SHAPES[sys.argv[2] if len(sys.argv) > 2 else "llama3-8b"]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for T in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,16,64,256,1024,4096").split(",")]:
     for name, n, k in shapes:
@@ -40,12 +45,12 @@ for T in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,16,64,256,10
             ref = lambda: torch.matmul(x, torch.cat([w, w2]).T)  # noqa: E731
         else:
             out = torch.zeros(T, n, device="cuda")
-            tiles = -(-n // 128) * -(-T // 128)
-            split = max(1, min(148 // max(tiles, 1), max(1, (k // 64) // 4)))
+            split = gemm_split(n, k, T)        # the executor's policy (llama.gemm_split)
             f = lambda: N.check(lib.lp_gemm_bf16(P(w), n, k, P(x), T, P(out), n, 0, split, None))  # noqa: E731
             flops, wbytes = 2 * T * n * k, 2 * n * k
             ref = lambda: torch.matmul(x, w.T)  # noqa: E731
         ms = timeit(f)
         ms_ref = timeit(ref)
-        print(f"T={T:5d} {name:8s} N={n:6d} K={k:6d}  ours {ms*1e3:8.1f} us  {wbytes/ms/1e6:7.0f} GB/s(w)  "
+        split_s = f"split={split}" if name != "gate_up" else "       "
+        print(f"T={T:5d} {name:8s} N={n:6d} K={k:6d} {split_s} ours {ms*1e3:8.1f} us  {wbytes/ms/1e6:7.0f} GB/s(w)  "
               f"{flops/ms/1e9:7.1f} TF/s | cuBLAS {ms_ref*1e3:8.1f} us {flops/ms_ref/1e9:7.1f} TF/s", flush=True)
