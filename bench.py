@@ -16,7 +16,11 @@ pinned DMA on the copy engines, NVLink relays in the multicast kernel).
 metric/value: aggregate delivered GB/s = N x model bytes / max-over-ranks
 device time of one scale-out (CUDA events around it on its stream).  At N >= 2
 the line also carries the GPU-sourced multicast (Llama-3-8B, GPU0 -> N-1
-peers, b = 32; BASELINE configs[1] at N = 8) as "gpu_source".
+peers, b = 32; BASELINE configs[1] at N = 8) as "gpu_source"; at N >= 3
+"execute_while_load" (Llama-3-8B, 2 GPU sources, λPipe pipelines serving a
+burst while the rest receive; tokens/s + TTFT), at N >= 4
+"execute_while_load_70b" (BASELINE configs[3] shape) and "bursty_trace"
+(configs[4]: the reference's synthetic spike trace with repeated scale-outs).
 
 --impl reference: the reference has no data plane (pure-Python planner +
 cost-model simulator); its CPU path for this workload is the
@@ -218,6 +222,7 @@ def main():
     ap.add_argument("--no-serving", action="store_true")
     ap.add_argument("--requests", type=int, default=32)
     ap.add_argument("--no-burst", action="store_true")
+    ap.add_argument("--no-serving-70b", action="store_true")
     ap.add_argument("--burst-compress", type=float, default=60.0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -337,6 +342,7 @@ def main():
 
     # --- execute-while-load serving (tokens/s + TTFT during load) ------------
     serving = None
+    serving70 = None
     burst = None
     if distributed and N >= 3 and not args.no_serving:
         torch.cuda.synchronize()
@@ -353,6 +359,25 @@ def main():
                                    "(cross-device pipelines); other ranks idle at a barrier")
             except Exception as e:  # noqa: BLE001
                 serving = {"error": f"{type(e).__name__}: {e}"}
+            if N >= 4 and not args.no_serving_70b:
+                # BASELINE configs[3]: Llama-3-70B (141 GB per replica) with λPipe
+                # pipelines over partial replicas while the multicast runs
+                import gc
+                gc.collect()
+                for d in range(N):
+                    with torch.cuda.device(d):
+                        torch.cuda.empty_cache()
+                try:
+                    serving70 = run_serving(N, model="llama3-70b", k=2, blocks=16, requests=16, executor="kernel",
+                                            pull_ctas=64)
+                    serving70["note"] = ("in-kernel multicast (64 CTAs per receiver) beside serving; rank 0 drives "
+                                         "all N GPUs")
+                except Exception as e:  # noqa: BLE001
+                    serving70 = {"error": f"{type(e).__name__}: {e}"}
+                gc.collect()
+                for d in range(N):
+                    with torch.cuda.device(d):
+                        torch.cuda.empty_cache()
             if not args.no_burst:
                 from burst_bench import run_burst
                 try:
@@ -428,6 +453,8 @@ def main():
             line["gpu_source"] = gpu_source
         if serving:
             line["execute_while_load"] = serving
+        if serving70:
+            line["execute_while_load_70b"] = serving70
         if burst:
             line["bursty_trace"] = burst
         print(json.dumps(line), flush=True)

@@ -59,35 +59,48 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16*
 // qkv: [T, (H + 2*KV) * hd] fp32.  HF Llama rotate_half RoPE: element j < hd/2
 // pairs with j + hd/2 at angle pos * theta^(-2j/hd).
 // q_out [T, H*hd] bf16; k/v appended to cache[seq][kv][pos][hd] bf16.
-__global__ void rope_kv_kernel(const float* __restrict__ qkv, int H, int KV, int hd, const int32_t* __restrict__ pos,
-                               const int32_t* __restrict__ seq, float theta, __nv_bfloat16* __restrict__ q_out,
-                               __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache,
-                               int64_t max_len) {
+//
+// One CTA per token: the angle table (cos, sin of pos * theta^(-2j/hd), j < hd/2)
+// depends only on the token's position, so it is computed once into smem and
+// shared by all H + KV rotated heads (a CTA per (token, head) recomputed it
+// per head: 87 us per 70B prefill layer at T = 1024); v heads are copied.
+constexpr int ROPE_THREADS = 256;
+constexpr int ROPE_MAX_HALF = 128;
+__global__ void __launch_bounds__(ROPE_THREADS) rope_kv_kernel(
+    const float* __restrict__ qkv, int H, int KV, int hd, const int32_t* __restrict__ pos,
+    const int32_t* __restrict__ seq, float theta, __nv_bfloat16* __restrict__ q_out,
+    __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache, int64_t max_len) {
   lp::pdl_wait();
   lp::pdl_trigger();
-  // grid (T, H + 2*KV): one CTA per (token, head); v heads are copied
   const int t = blockIdx.x;
-  const int head = blockIdx.y;
   const int p = pos[t];
   const int sq = seq[t];
   const int half = hd / 2;
-  const float* src = qkv + ((int64_t)t * (H + 2 * KV) + head) * hd;
-  if (head >= H + KV) {
-    const int kh = head - H - KV;
-    __nv_bfloat16* dst = v_cache + (((int64_t)sq * KV + kh) * max_len + p) * hd;
-    for (int j = threadIdx.x; j < hd; j += blockDim.x) dst[j] = __float2bfloat16_rn(src[j]);
-    return;
-  }
-  __nv_bfloat16* dst = head < H ? q_out + ((int64_t)t * H + head) * hd
-                                : k_cache + (((int64_t)sq * KV + (head - H)) * max_len + p) * hd;
+  __shared__ float s_cos[ROPE_MAX_HALF], s_sin[ROPE_MAX_HALF];
   const float l2t = log2f(theta);
   for (int j = threadIdx.x; j < half; j += blockDim.x) {
     const float inv = exp2f(-2.0f * (float)j / (float)hd * l2t);
     float sn, cs;
     sincosf((float)p * inv, &sn, &cs);
-    const float a = src[j], b = src[j + half];
+    s_cos[j] = cs;
+    s_sin[j] = sn;
+  }
+  __syncthreads();
+  const float* row = qkv + (int64_t)t * (H + 2 * KV) * hd;
+  const int rot = (H + KV) * half;                       // rotated (q and k) pairs
+  for (int i = threadIdx.x; i < rot; i += blockDim.x) {
+    const int head = i / half, j = i % half;
+    const float* src = row + (int64_t)head * hd;
+    __nv_bfloat16* dst = head < H ? q_out + ((int64_t)t * H + head) * hd
+                                  : k_cache + (((int64_t)sq * KV + (head - H)) * max_len + p) * hd;
+    const float a = src[j], b = src[j + half], cs = s_cos[j], sn = s_sin[j];
     dst[j] = __float2bfloat16_rn(a * cs - b * sn);
     dst[j + half] = __float2bfloat16_rn(b * cs + a * sn);
+  }
+  const float* vsrc = row + (int64_t)(H + KV) * hd;
+  for (int i = threadIdx.x; i < KV * hd; i += blockDim.x) {
+    const int kh = i / hd, j = i % hd;
+    v_cache[(((int64_t)sq * KV + kh) * max_len + p) * hd + j] = __float2bfloat16_rn(vsrc[i]);
   }
 }
 
@@ -121,27 +134,42 @@ __device__ __forceinline__ void load_v(const __nv_bfloat16* p, float (&f)[4]) {
   }
 }
 
-template <int HD>
+//
+// ROW_PER_WARP (many rows, e.g. prefill): each warp owns one row and walks all
+// of its key chunks — no idle warps on short contexts, no cross-warp merge;
+// otherwise (decode: few rows, long contexts) the CTA's warps split one row's
+// keys and merge through smem.
+template <int HD, bool ROW_PER_WARP>
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
-    int H, int KV, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
+    int T, int H, int KV, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
   constexpr int PER = HD / 32;   // output dims per lane
   lp::pdl_wait();
   lp::pdl_trigger();
-  const int t = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = ROW_PER_WARP ? blockIdx.x * ATT_WARPS + warp : blockIdx.x;
+  if (ROW_PER_WARP && t >= T) return;
   const int kh = blockIdx.y;
   const int G = H / KV;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = pos[t] + 1;
   const __nv_bfloat16* kb = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
   const __nv_bfloat16* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
-  __shared__ float sq[MAX_G][HD];
-  for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
-    const int g = i / HD, dd = i % HD;
-    sq[g][dd] = __bfloat162float(q[((int64_t)t * H + kh * G + g) * HD + dd]) * scale;
+  __shared__ float sq_all[ROW_PER_WARP ? ATT_WARPS : 1][MAX_G][HD];
+  float (&sq)[MAX_G][HD] = sq_all[ROW_PER_WARP ? warp : 0];
+  if (ROW_PER_WARP) {
+    for (int i = lane; i < G * HD; i += 32) {
+      const int g = i / HD, dd = i % HD;
+      sq[g][dd] = __bfloat162float(q[((int64_t)t * H + kh * G + g) * HD + dd]) * scale;
+    }
+    __syncwarp();
+  } else {
+    for (int i = threadIdx.x; i < G * HD; i += blockDim.x) {
+      const int g = i / HD, dd = i % HD;
+      sq[g][dd] = __bfloat162float(q[((int64_t)t * H + kh * G + g) * HD + dd]) * scale;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   float m[MAX_G], l[MAX_G], acc[MAX_G][PER];
 #pragma unroll
   for (int g = 0; g < MAX_G; ++g) {
@@ -150,7 +178,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
 #pragma unroll
     for (int i = 0; i < PER; ++i) acc[g][i] = 0.f;
   }
-  for (int c0 = warp * 32; c0 < L; c0 += ATT_WARPS * 32) {
+  for (int c0 = ROW_PER_WARP ? 0 : warp * 32; c0 < L; c0 += ROW_PER_WARP ? 32 : ATT_WARPS * 32) {
     const int j = c0 + lane;
     const bool live = j < L;
     float s[MAX_G];
@@ -214,6 +242,17 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
         }
       }
     }
+  }
+  if constexpr (ROW_PER_WARP) {
+#pragma unroll
+    for (int g = 0; g < MAX_G; ++g) {
+      if (g >= G) break;
+      const float inv = 1.0f / l[g];
+#pragma unroll
+      for (int i = 0; i < PER; ++i)
+        out[((int64_t)t * H + kh * G + g) * HD + lane * PER + i] = __float2bfloat16_rn(acc[g][i] * inv);
+    }
+    return;
   }
   __shared__ float sm_m[ATT_WARPS][MAX_G], sm_l[ATT_WARPS][MAX_G];
   __shared__ float sm_acc[ATT_WARPS][MAX_G][HD];
@@ -355,7 +394,8 @@ int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim,
                void* stream) {
   LP_CHECK(qkv && pos && seq && q_out && k_cache && v_cache && T > 0, "lp_rope_kv: bad arguments");
   LP_CHECK(n_kv > 0 && n_heads % n_kv == 0 && head_dim % 2 == 0, "lp_rope_kv: bad head shape");
-  LP_CUDA(lp::launch(rope_kv_kernel, dim3((unsigned)T, (unsigned)(n_heads + 2 * n_kv)), dim3(64), 0, (cudaStream_t)stream, qkv, n_heads, n_kv,
+  LP_CHECK(head_dim / 2 <= ROPE_MAX_HALF, "lp_rope_kv: head_dim > %d", 2 * ROPE_MAX_HALF);
+  LP_CUDA(lp::launch(rope_kv_kernel, dim3((unsigned)T), dim3(ROPE_THREADS), 0, (cudaStream_t)stream, qkv, n_heads, n_kv,
                      head_dim, pos, seq, theta, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
                      (__nv_bfloat16*)v_cache, max_len));
   return 0;
@@ -367,18 +407,27 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
   LP_CHECK(q && k_cache && v_cache && pos && seq && out && T > 0, "lp_attention: bad arguments");
   LP_CHECK(n_kv > 0 && n_heads % n_kv == 0 && n_heads / n_kv <= MAX_G, "lp_attention: GQA group > %d", MAX_G);
   LP_CHECK(head_dim % 32 == 0 && head_dim <= 128, "lp_attention: head_dim must be 32..128, multiple of 32");
-  dim3 grid((unsigned)T, (unsigned)n_kv);
   const __nv_bfloat16 *qq = (const __nv_bfloat16*)q, *kk = (const __nv_bfloat16*)k_cache,
                       *vv = (const __nv_bfloat16*)v_cache;
   __nv_bfloat16* oo = (__nv_bfloat16*)out;
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 blk(ATT_WARPS * 32);
+  // many rows (prefill): a warp per row; few rows (decode): a CTA per row
+  const bool rpw = T * n_kv >= 1024;
+  const dim3 grid(rpw ? (unsigned)((T + ATT_WARPS - 1) / ATT_WARPS) : (unsigned)T, (unsigned)n_kv);
+  const int Ti = (int)T;
+#define LP_ATT(HDV)                                                                                              \
+  (rpw ? lp::launch(attention_kernel<HDV, true>, grid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv, max_len, \
+                    scale, oo)                                                                                   \
+       : lp::launch(attention_kernel<HDV, false>, grid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv,        \
+                    max_len, scale, oo))
   switch (head_dim) {
-    case 32: LP_CUDA(lp::launch(attention_kernel<32>, grid, blk, 0, s, qq, kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)); break;
-    case 64: LP_CUDA(lp::launch(attention_kernel<64>, grid, blk, 0, s, qq, kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)); break;
-    case 96: LP_CUDA(lp::launch(attention_kernel<96>, grid, blk, 0, s, qq, kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)); break;
-    default: LP_CUDA(lp::launch(attention_kernel<128>, grid, blk, 0, s, qq, kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)); break;
+    case 32: LP_CUDA(LP_ATT(32)); break;
+    case 64: LP_CUDA(LP_ATT(64)); break;
+    case 96: LP_CUDA(LP_ATT(96)); break;
+    default: LP_CUDA(LP_ATT(128)); break;
   }
+#undef LP_ATT
   return 0;
 }
 

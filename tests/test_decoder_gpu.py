@@ -58,17 +58,19 @@ def test_gemm_swiglu_matches_fp32(n, k, t):
     assert ((out.float() - ref).abs() / (ref.abs() + 0.1)).max().item() < 0.05
 
 
-@pytest.mark.parametrize("hd,H,KV,ctx", [(128, 32, 8, [1, 150, 37, 300]), (64, 4, 2, [5, 129, 64]),
-                                          (128, 64, 8, [200, 17]), (128, 8, 8, [33, 96])])
-def test_attention_matches_fp32(hd, H, KV, ctx):
+@pytest.mark.parametrize("hd,H,KV,ctx,run", [(128, 32, 8, [1, 150, 37, 300], 40), (64, 4, 2, [5, 129, 64], 40),
+                                              (128, 64, 8, [200, 17], 40), (128, 8, 8, [33, 96], 40),
+                                              (128, 64, 8, [300, 5], 200), (64, 4, 2, [600], 520)])
+def test_attention_matches_fp32(hd, H, KV, ctx, run):
     """Ragged causal GQA attention (decode rows at arbitrary positions and a
-    prefill-style run of consecutive positions) vs a torch fp32 softmax."""
+    prefill-style run of ``run`` consecutive positions) vs a torch fp32
+    softmax; T x KV >= 1024 selects the warp-per-row (prefill) variant."""
     import torch
     g = torch.Generator(device="cuda").manual_seed(hd + H + len(ctx))
     seqs, max_len = len(ctx), max(ctx) + 8
     kc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
     vc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
-    pos = [c - 1 for c in ctx] + list(range(ctx[0] - 1, max(ctx[0] - 40, -1), -1))
+    pos = [c - 1 for c in ctx] + list(range(ctx[0] - 1, max(ctx[0] - run, -1), -1))
     seq = list(range(seqs)) + [0] * (len(pos) - seqs)
     T = len(pos)
     q = torch.randn(T, H, hd, device="cuda", generator=g).to(torch.bfloat16)
