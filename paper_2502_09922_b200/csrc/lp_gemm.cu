@@ -439,6 +439,253 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair variant for prefill (tcgen05.mma.cta_group::2).  At 128 x BT x 16
+// per CTA the MMA reads 96 B/clk of smem operands while TMA writes another
+// 96 B/clk into the same smem — more than the SM's smem bandwidth, which is
+// what held the single-CTA kernel's tensor pipe at ~65 % (ncu,
+// gemm_prefill_qkv_T4096_full_r01.csv).  A cluster of two CTAs on one TPC
+// computes a 256 x BT tile: each CTA stages its own 128 weight rows and HALF
+// of the token tile (BT/2 rows); the leader's single thread issues
+// M = 256 MMAs that read both CTAs' smem, and every CTA's TMEM receives its
+// 128 rows x BT accumulator — per-SM smem traffic per MMA is halved for B.
+//   * both CTAs' TMA loads complete on the LEADER's full barrier
+//     (.cta_group::2 TMA, barrier address mapped to rank 0); the leader
+//     expects the pair's bytes;
+//   * the leader's commits arrive on both CTAs' empty / accumulator-full
+//     barriers (multicast::cluster, mask 0b11);
+//   * both CTAs' epilogue warps release the accumulator on the leader's
+//     tempty barrier (remote mbarrier.arrive.release.cluster).
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(lp::smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(lp::smem_u32(smem_dst)),
+      "l"(map), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                           uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          lp::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+template <int N>
+__host__ __device__ constexpr uint32_t idesc2_bf16_f32() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+template <int BT, int EPI>
+struct Cfg2 {
+  static constexpr int A_BYTES = BM * BK * 2;                 // this CTA's 128 weight rows
+  static constexpr int B_BYTES = (BT / 2) * BK * 2;           // this CTA's half of the token tile
+  static constexpr int NA = (EPI == EPI_SWIGLU) ? 2 : 1;
+  static constexpr int STAGE_BYTES = NA * A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int ACC_COLS = NA * BT;
+  static constexpr int NBUF = 2 * ACC_COLS <= 512 ? 2 : 1;
+  static constexpr int TC = NBUF * ACC_COLS;
+  static constexpr int TCOLS = TC <= 32 ? 32 : TC <= 64 ? 64 : TC <= 128 ? 128 : TC <= 256 ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;
+};
+
+template <int BT, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmW2,
+                     const __grid_constant__ CUtensorMap tmXh, const GemmArgs args) {
+  using C = Cfg2<BT, EPI>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[C::STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[C::STAGES];
+  __shared__ __align__(8) uint64_t tfull[2];
+  __shared__ __align__(8) uint64_t tempty[2];
+  __shared__ uint32_t tmem_base_smem;
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int tiles_n2 = (args.tiles_n + 1) >> 1;            // 256-row pair tiles
+  const int total = tiles_n2 * args.tiles_t * args.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      lp::mbar_init(&full_bar[s], 1);
+      lp::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      lp::mbar_init(&tfull[a], 1);
+      lp::mbar_init(&tempty[a], 8);     // 4 epilogue warps x 2 CTAs
+    }
+    lp::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     lp::smem_u32(&tmem_base_smem)),
+                 "r"(C::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXh) : "memory");
+    if (EPI == EPI_SWIGLU) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW2) : "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_smem;
+
+  auto tile_coords = [&](int tile, int& n0, int& t0, int& kb0, int& nkb) {
+    const int nt = tile % tiles_n2;
+    const int rest = tile / tiles_n2;
+    const int tt = rest % args.tiles_t;
+    const int z = rest / args.tiles_t;
+    n0 = nt * 2 * BM + (int)rank * BM;
+    t0 = tt * BT;
+    kb0 = z * args.kb_per_split;
+    nkb = min(args.k_blocks, kb0 + args.kb_per_split) - kb0;
+  };
+
+  if (threadIdx.x == 0) lp::pdl_trigger();
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    lp::pdl_wait();
+    int it = 0;
+    for (int tile = cid; tile < total; tile += nclusters) {
+      int n0, t0, kb0, nkb;
+      tile_coords(tile, n0, t0, kb0, nkb);
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % C::STAGES;
+        lp::mbar_wait(&empty_bar[s], ((it / C::STAGES) & 1) ^ 1);
+        if (rank == 0) lp::mbar_expect_tx(&full_bar[s], 2 * C::STAGE_BYTES);
+        const uint32_t lbar = mapa_rank(lp::smem_u32(&full_bar[s]), 0);
+        uint8_t* st = smem + s * C::STAGE_BYTES;
+        const int kc = (kb0 + i) * BK;
+        tma_load_2d_pair(st, &tmW, lbar, kc, n0);
+        if (EPI == EPI_SWIGLU) tma_load_2d_pair(st + C::A_BYTES, &tmW2, lbar, kc, n0);
+        tma_load_2d_pair(st + C::NA * C::A_BYTES, &tmXh, lbar, kc, t0 + (int)rank * (BT / 2));
+      }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    constexpr uint32_t idesc = idesc2_bf16_f32<BT>();
+    int it = 0, li = 0;
+    for (int tile = cid; tile < total; tile += nclusters, ++li) {
+      int n0, t0, kb0, nkb;
+      tile_coords(tile, n0, t0, kb0, nkb);
+      const int a = li % C::NBUF;
+      mbar_wait_cluster(&tempty[a], ((li / C::NBUF) & 1) ^ 1);   // both CTAs drained this accumulator
+      tc_fence_after();
+      const uint32_t acc_base = tmem + a * C::ACC_COLS;
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % C::STAGES;
+        lp::mbar_wait(&full_bar[s], (it / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = lp::smem_u32(smem + s * C::STAGE_BYTES);
+        const uint32_t sb = sa + C::NA * C::A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          umma2_bf16(acc_base, smem_desc_sw128(sa + kk * 32), smem_desc_sw128(sb + kk * 32), idesc, acc);
+          if (EPI == EPI_SWIGLU)
+            umma2_bf16(acc_base + BT, smem_desc_sw128(sa + C::A_BYTES + kk * 32), smem_desc_sw128(sb + kk * 32),
+                       idesc, acc);
+        }
+        umma2_commit_both(&empty_bar[s]);
+      }
+      umma2_commit_both(&tfull[a]);
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue (both CTAs, own 128 rows) ----------------
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t leader_tempty0 = mapa_rank(lp::smem_u32(&tempty[0]), 0);
+    const uint32_t leader_tempty1 = mapa_rank(lp::smem_u32(&tempty[1]), 0);
+    int li = 0;
+    for (int tile = cid; tile < total; tile += nclusters, ++li) {
+      int n0, t0, kb0, nkb;
+      tile_coords(tile, n0, t0, kb0, nkb);
+      const int a = li % C::NBUF;
+      lp::mbar_wait(&tfull[a], (li / C::NBUF) & 1);
+      tc_fence_after();
+      const int n = n0 + row;
+      constexpr int CH = BT < 32 ? BT : 32;
+      for (int c = 0; c < BT; c += CH) {
+        uint32_t v[32], u[32];
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * C::ACC_COLS + c;
+        if (CH == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
+        if (EPI == EPI_SWIGLU) {
+          if (CH == 32) tmem_ld32(taddr + BT, u); else tmem_ld16(taddr + BT, u);
+        }
+        tmem_wait_ld();
+        if (n < args.n_rows) {
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            const int t = t0 + c + j;
+            if (t >= args.tokens) break;
+            const float x = __uint_as_float(v[j]);
+            if (EPI == EPI_ADD_F32) {
+              float* o = (float*)args.out + (int64_t)t * args.ldo + n;
+              if (args.atomic) atomicAdd(o, x); else *o += x;
+            } else if (EPI == EPI_STORE_F32) {
+              ((float*)args.out)[(int64_t)t * args.ldo + n] = x;
+            } else {
+              const float up = __uint_as_float(u[j]);
+              ((__nv_bfloat16*)args.out)[(int64_t)t * args.ldo + n] =
+                  __float2bfloat16_rn(x / (1.0f + __expf(-x)) * up);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(a == 0 ? leader_tempty0 : leader_tempty1);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side: tensor maps (driver entry point via the runtime) + dispatch
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -488,6 +735,13 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
     streamk = (e && e[0] == '1') ? 1 : 0;
   }
   const bool persistent = T > 64 || streamk;
+  // CTA pairs for prefill (LP_GEMM_PAIR=0 selects the single-CTA kernel)
+  static int pair_env = -1;
+  if (pair_env < 0) {
+    const char* e = getenv("LP_GEMM_PAIR");
+    pair_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool pair = T > 64 && pair_env;
   static uint64_t attr_set = 0;   // per-device bit: the smem opt-in is a per-device function attribute
   int dev = 0;
   LP_CUDA(cudaGetDevice(&dev));
@@ -495,6 +749,9 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
     LP_CUDA(cudaFuncSetAttribute(gemm_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     LP_CUDA(cudaFuncSetAttribute(gemm_persistent_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM));
+    if constexpr (BT >= 32)
+      LP_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<BT, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Cfg2<BT, EPI>::SMEM));
     attr_set |= 1ull << dev;
   }
   GemmArgs a;
@@ -511,6 +768,19 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
   a.tiles_n = (int)((N + BM - 1) / BM);
   a.tiles_t = (int)((T + BT - 1) / BT);
   a.splits = splits;
+  if constexpr (BT >= 32) {
+    if (pair) {
+      CUtensorMap mxh;
+      if (make_map(&mxh, X, T, K, BT / 2) != 0) return -1;
+      static int sms2 = 0;
+      if (!sms2) LP_CUDA(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev));
+      const int total = ((a.tiles_n + 1) / 2) * a.tiles_t * a.splits;
+      const int clusters = total < sms2 / 2 ? total : sms2 / 2;
+      LP_CUDA(lp::launch(gemm_pair_kernel<BT, EPI>, dim3(2 * clusters), dim3(THREADS), Cfg2<BT, EPI>::SMEM, s, mw,
+                         mw2, mxh, a));
+      return 0;
+    }
+  }
   if (persistent) {
     static int sms = 0;
     if (!sms) LP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

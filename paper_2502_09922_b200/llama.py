@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import time
 
 from . import _native as N
@@ -31,6 +32,7 @@ from .engine import device_view
 from .image import ImageLayout
 
 _SMS = 148
+GEMM_PAIR = os.environ.get("LP_GEMM_PAIR", "1") != "0"   # mirrors lp_gemm.cu's switch
 
 
 def _vp(x):
@@ -47,6 +49,7 @@ def _cur_stream(stream):
 
 
 SMS = 148
+GEMM_PAIR = os.environ.get("LP_GEMM_PAIR", "1") != "0"   # mirrors lp_gemm.cu's switch
 
 
 def gemm_token_tile(tokens: int) -> int:
@@ -66,11 +69,16 @@ def gemm_split(n_rows: int, k: int, tokens: int) -> int:
     slots), discounted 2 % per extra split — e.g. QKV at T = 256 has only 48 tiles of 128 x 256, so
     48 of 148 SMs would work without a 3-way split.  Each split keeps >= 8
     k-blocks of 64."""
-    tiles = -(-n_rows // 128) * -(-tokens // gemm_token_tile(tokens))
     kb = -(-k // 64)
     if tokens <= 64:
+        tiles = -(-n_rows // 128) * -(-tokens // gemm_token_tile(tokens))
         return max(1, min(round(160 / max(tiles, 1)), max(1, kb // 4)))
-    if tiles >= 2 * SMS:
+    # prefill runs on CTA pairs (lp_gemm.cu gemm_pair_kernel): 256-row tiles
+    # over SMS / 2 cluster slots
+    slots = SMS // 2 if GEMM_PAIR else SMS
+    rows = 256 if GEMM_PAIR else 128
+    tiles = -(-n_rows // rows) * -(-tokens // gemm_token_tile(tokens))
+    if tiles >= 2 * slots:
         # >= 2 waves: tiles finish at staggered times, so quantisation costs
         # less than modelled, while shorter K per item exposes the red.add
         # epilogue (T = 4096 QKV: 167 us unsplit vs 192 us at 3 splits)
@@ -80,7 +88,7 @@ def gemm_split(n_rows: int, k: int, tokens: int) -> int:
         if split > 1 and kb // split < 8:
             break
         items = tiles * split
-        eff = items / (-(-items // SMS) * SMS)
+        eff = items / (-(-items // slots) * slots)
         score = eff * (1.0 - 0.02 * (split - 1))    # each split re-adds T x N partial sums
         if score > best_score + 1e-9:
             best, best_score = split, score
