@@ -134,6 +134,82 @@ __device__ __forceinline__ void load_v(const __nv_bfloat16* p, float (&f)[4]) {
   }
 }
 
+// Online-softmax attention of one query row (G heads, q pre-scaled in sq)
+// over keys c_begin, c_begin + c_step, ... (32-key chunks, lane per key) of
+// K/V rows at kb / vb with the given row strides (global cache or smem copy).
+template <int HD>
+__device__ __forceinline__ void att_chunks(const float (&sq)[MAX_G][HD], const __nv_bfloat16* kb, int kstride,
+                                           const __nv_bfloat16* vb, int vstride, int G, int L, int c_begin,
+                                           int c_step, int lane, float (&m)[MAX_G], float (&l)[MAX_G],
+                                           float (&acc)[MAX_G][HD / 32]) {
+  constexpr int PER = HD / 32;
+  for (int c0 = c_begin; c0 < L; c0 += c_step) {
+    const int j = c0 + lane;
+    const bool live = j < L;
+    float s[MAX_G];
+#pragma unroll
+    for (int g = 0; g < MAX_G; ++g) s[g] = 0.f;
+    if (live) {
+      const int4* kr = reinterpret_cast<const int4*>(kb + (int64_t)j * kstride);
+      int4 raw[HD / 8];
+#pragma unroll
+      for (int v8 = 0; v8 < HD / 8; ++v8) raw[v8] = kr[v8];
+#pragma unroll
+      for (int v8 = 0; v8 < HD / 8; ++v8) {
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[v8]);
+        float kf[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          kf[2 * e] = f.x;
+          kf[2 * e + 1] = f.y;
+        }
+#pragma unroll
+        for (int g = 0; g < MAX_G; ++g) {
+          if (g < G) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s[g] += sq[g][v8 * 8 + e] * kf[e];
+          }
+        }
+      }
+    }
+    float p[MAX_G];
+#pragma unroll
+    for (int g = 0; g < MAX_G; ++g) {
+      p[g] = 0.f;
+      if (g >= G) continue;
+      const float cm = warp_max(live ? s[g] : -INFINITY);
+      const float mn = fmaxf(m[g], cm);
+      const float corr = __expf(m[g] - mn);
+      p[g] = live ? __expf(s[g] - mn) : 0.f;
+      l[g] = l[g] * corr + warp_sum(p[g]);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) acc[g][i] *= corr;
+      m[g] = mn;
+    }
+    const int nk = min(32, L - c0);
+    for (int j0 = 0; j0 < nk; j0 += PV_BATCH) {
+      float vf[PV_BATCH][4];
+#pragma unroll
+      for (int b = 0; b < PV_BATCH; ++b) {
+        const int key = c0 + min(j0 + b, nk - 1);     // clamped: dead keys have p = 0
+        load_v<PER>(vb + (int64_t)key * vstride + lane * PER, vf[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < PV_BATCH; ++b) {
+#pragma unroll
+        for (int g = 0; g < MAX_G; ++g) {
+          if (g >= G) break;
+          const float pj = __shfl_sync(0xffffffffu, p[g], (j0 + b) & 31);
+          const float w = (j0 + b < nk) ? pj : 0.f;
+#pragma unroll
+          for (int i = 0; i < PER; ++i) acc[g][i] += w * vf[b][i];
+        }
+      }
+    }
+  }
+}
+
 //
 // ROW_PER_WARP (many rows, e.g. prefill): each warp owns one row and walks all
 // of its key chunks — no idle warps on short contexts, no cross-warp merge;
@@ -178,71 +254,8 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
 #pragma unroll
     for (int i = 0; i < PER; ++i) acc[g][i] = 0.f;
   }
-  for (int c0 = ROW_PER_WARP ? 0 : warp * 32; c0 < L; c0 += ROW_PER_WARP ? 32 : ATT_WARPS * 32) {
-    const int j = c0 + lane;
-    const bool live = j < L;
-    float s[MAX_G];
-#pragma unroll
-    for (int g = 0; g < MAX_G; ++g) s[g] = 0.f;
-    if (live) {
-      const int4* kr = reinterpret_cast<const int4*>(kb + (int64_t)j * HD);
-      int4 raw[HD / 8];
-#pragma unroll
-      for (int v8 = 0; v8 < HD / 8; ++v8) raw[v8] = kr[v8];
-#pragma unroll
-      for (int v8 = 0; v8 < HD / 8; ++v8) {
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[v8]);
-        float kf[8];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(h2[e]);
-          kf[2 * e] = f.x;
-          kf[2 * e + 1] = f.y;
-        }
-#pragma unroll
-        for (int g = 0; g < MAX_G; ++g) {
-          if (g < G) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) s[g] += sq[g][v8 * 8 + e] * kf[e];
-          }
-        }
-      }
-    }
-    float p[MAX_G];
-#pragma unroll
-    for (int g = 0; g < MAX_G; ++g) {
-      p[g] = 0.f;
-      if (g >= G) continue;
-      const float cm = warp_max(live ? s[g] : -INFINITY);
-      const float mn = fmaxf(m[g], cm);
-      const float corr = __expf(m[g] - mn);
-      p[g] = live ? __expf(s[g] - mn) : 0.f;
-      l[g] = l[g] * corr + warp_sum(p[g]);
-#pragma unroll
-      for (int i = 0; i < PER; ++i) acc[g][i] *= corr;
-      m[g] = mn;
-    }
-    const int nk = min(32, L - c0);
-    for (int j0 = 0; j0 < nk; j0 += PV_BATCH) {
-      float vf[PV_BATCH][4];
-#pragma unroll
-      for (int b = 0; b < PV_BATCH; ++b) {
-        const int key = c0 + min(j0 + b, nk - 1);     // clamped: dead keys have p = 0
-        load_v<PER>(vb + (int64_t)key * HD + lane * PER, vf[b]);
-      }
-#pragma unroll
-      for (int b = 0; b < PV_BATCH; ++b) {
-#pragma unroll
-        for (int g = 0; g < MAX_G; ++g) {
-          if (g >= G) break;
-          const float pj = __shfl_sync(0xffffffffu, p[g], (j0 + b) & 31);
-          const float w = (j0 + b < nk) ? pj : 0.f;
-#pragma unroll
-          for (int i = 0; i < PER; ++i) acc[g][i] += w * vf[b][i];
-        }
-      }
-    }
-  }
+  att_chunks<HD>(sq, kb, HD, vb, HD, G, L, ROW_PER_WARP ? 0 : warp * 32, ROW_PER_WARP ? 32 : ATT_WARPS * 32, lane,
+                 m, l, acc);
   if constexpr (ROW_PER_WARP) {
 #pragma unroll
     for (int g = 0; g < MAX_G; ++g) {
@@ -279,6 +292,228 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
       num += sm_acc[w][g][dcol] * f;
     }
     out[((int64_t)t * H + kh * G + g) * HD + dcol] = __float2bfloat16_rn(num / den);
+  }
+}
+
+// Prefill on the tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate):
+// FlashAttention-2 style.  A CTA takes 16 consecutive rows and one kv head;
+// each of its 4 warps one query head of the GQA group (grid z covers groups
+// > 4).  When the 16 rows share one sequence (a request's prompt tokens are
+// consecutive rows), that sequence's keys are streamed through smem in
+// 64-key chunks: S = Q K^T (Q fragments in registers, K fragments straight
+// from padded smem rows), per-row causal mask pos[row], online softmax in
+// registers, P reused as the A operand of P V (V fragments via
+// ldmatrix.trans).  Tiles mixing sequences fall back to the CUDA-core row
+// path.  Replaces a lane-per-key CUDA-core loop that ran at ~9 % of FMA
+// peak (8B prefill, 2048 rows: 340 us per layer).
+constexpr int MMA_ROWS = 16;
+constexpr int MMA_KEYS = 64;
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
+    const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
+    int T, int H, int KV, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
+  constexpr int KS = HD + 8;                 // padded smem row (elements): conflict-free fragments
+  constexpr int KSTEPS = HD / 16;            // QK^T k-steps
+  constexpr int DT = HD / 8;                 // PV n-tiles
+  __shared__ __align__(16) __nv_bfloat16 Ks[MMA_KEYS][KS];
+  __shared__ __align__(16) __nv_bfloat16 Vs[MMA_KEYS][KS];
+  __shared__ int s_same, s_len, s_pos[MMA_ROWS];
+  lp::pdl_wait();
+  lp::pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kh = blockIdx.y;
+  const int G = H / KV;
+  const int t0 = blockIdx.x * MMA_ROWS;
+  const int t1 = min(T, t0 + MMA_ROWS);
+  if (threadIdx.x == 0) {
+    const int s0 = seq[t0];
+    int same = 1, len = 0;
+    for (int t = t0; t < t1; ++t) {
+      same &= seq[t] == s0;
+      len = max(len, pos[t] + 1);
+    }
+    s_same = same;
+    s_len = len;
+  }
+  if (threadIdx.x < MMA_ROWS) s_pos[threadIdx.x] = (t0 + (int)threadIdx.x < T) ? pos[t0 + threadIdx.x] : -1;
+  __syncthreads();
+  if (!s_same) {
+    // mixed sequences: CUDA-core rows (all G heads per row), z == 0 CTAs only
+    if (blockIdx.z != 0) return;
+    constexpr int PER = HD / 32;
+    static_assert(sizeof(float) * ATT_WARPS * MAX_G * HD <= sizeof(__nv_bfloat16) * MMA_KEYS * KS,
+                  "fallback q staging must fit the K tile");
+    float (&sq)[MAX_G][HD] = reinterpret_cast<float (*)[MAX_G][HD]>(&Ks[0][0])[warp];
+    for (int t = t0 + warp; t < t1; t += ATT_WARPS) {
+      for (int i = lane; i < G * HD; i += 32) {
+        const int g = i / HD, dd = i % HD;
+        sq[g][dd] = __bfloat162float(q[((int64_t)t * H + kh * G + g) * HD + dd]) * scale;
+      }
+      __syncwarp();
+      float m[MAX_G], l[MAX_G], acc[MAX_G][PER];
+#pragma unroll
+      for (int g = 0; g < MAX_G; ++g) {
+        m[g] = -INFINITY;
+        l[g] = 0.f;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) acc[g][i] = 0.f;
+      }
+      const __nv_bfloat16* kb = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+      const __nv_bfloat16* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+      att_chunks<HD>(sq, kb, HD, vb, HD, G, pos[t] + 1, 0, 32, lane, m, l, acc);
+#pragma unroll
+      for (int g = 0; g < MAX_G; ++g) {
+        if (g >= G) break;
+        const float inv = 1.0f / l[g];
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+          out[((int64_t)t * H + kh * G + g) * HD + lane * PER + i] = __float2bfloat16_rn(acc[g][i] * inv);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  const int g = blockIdx.z * ATT_WARPS + warp;    // this warp's query head within the group
+  const bool active = g < G;
+  const int head = kh * G + (active ? g : 0);
+  const int r0 = lane >> 2, cq = (lane & 3) * 2;  // fragment row / column pair
+  // Q fragments (A operand, 16 rows x HD), rows past T are zero
+  uint32_t qa[KSTEPS][4];
+#pragma unroll
+  for (int ks = 0; ks < KSTEPS; ++ks) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {              // h: row r0 / r0 + 8
+      const int t = t0 + r0 + 8 * h;
+      const __nv_bfloat16* qr = q + ((int64_t)t * H + head) * HD + ks * 16 + cq;
+      qa[ks][h] = t < T ? *reinterpret_cast<const uint32_t*>(qr) : 0u;
+      qa[ks][2 + h] = t < T ? *reinterpret_cast<const uint32_t*>(qr + 8) : 0u;
+    }
+  }
+  const int prow[2] = {s_pos[r0], s_pos[r0 + 8]};
+  float o[DT][4];
+#pragma unroll
+  for (int i = 0; i < DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const float sl2 = scale * 1.4426950408889634f;  // softmax in base 2
+  const int len = s_len;
+  const __nv_bfloat16* kg = k_cache + ((int64_t)seq[t0] * KV + kh) * max_len * HD;
+  const __nv_bfloat16* vg = v_cache + ((int64_t)seq[t0] * KV + kh) * max_len * HD;
+  for (int c0 = 0; c0 < len; c0 += MMA_KEYS) {
+    const int nk = min(MMA_KEYS, len - c0);
+    constexpr int V8 = HD / 8;
+    for (int i = threadIdx.x; i < MMA_KEYS * V8; i += blockDim.x) {
+      const int r = i / V8, c = i % V8;
+      int4 kv = make_int4(0, 0, 0, 0), vv = kv;
+      if (r < nk) {
+        kv = reinterpret_cast<const int4*>(kg + (int64_t)(c0 + r) * HD)[c];
+        vv = reinterpret_cast<const int4*>(vg + (int64_t)(c0 + r) * HD)[c];
+      }
+      reinterpret_cast<int4*>(&Ks[r][0])[c] = kv;
+      reinterpret_cast<int4*>(&Vs[r][0])[c] = vv;
+    }
+    __syncthreads();
+    if (active) {
+      // S = Q K^T over this chunk: 8 n-tiles of 8 keys
+      float sc[MMA_KEYS / 8][4];
+#pragma unroll
+      for (int nt = 0; nt < MMA_KEYS / 8; ++nt) {
+        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+        const __nv_bfloat16* kr = &Ks[nt * 8 + r0][cq];
+#pragma unroll
+        for (int ks = 0; ks < KSTEPS; ++ks) {
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + ks * 16);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + ks * 16 + 8);
+          mma_bf16_16816(sc[nt], qa[ks], b0, b1);
+        }
+      }
+      // causal mask + online softmax (each thread: rows r0, r0 + 8; a quad shares a row)
+      float mnew[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < MMA_KEYS / 8; ++nt) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int key = c0 + nt * 8 + cq + e;
+            float v = sc[nt][2 * h + e] * sl2;
+            if (key > prow[h]) v = -INFINITY;
+            sc[nt][2 * h + e] = v;
+            mx = fmaxf(mx, v);
+          }
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        mnew[h] = fmaxf(mrow[h], mx);
+        const float corr = mnew[h] == -INFINITY ? 1.f : exp2f(mrow[h] - mnew[h]);
+        lrow[h] *= corr;
+#pragma unroll
+        for (int dt = 0; dt < DT; ++dt) {
+          o[dt][2 * h] *= corr;
+          o[dt][2 * h + 1] *= corr;
+        }
+        mrow[h] = mnew[h];
+      }
+      uint32_t pa[MMA_KEYS / 16][4];
+#pragma unroll
+      for (int nt = 0; nt < MMA_KEYS / 8; ++nt) {
+        float pv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int h = i >> 1;
+          pv[i] = mnew[h] == -INFINITY ? 0.f : exp2f(sc[nt][i] - mnew[h]);
+          lrow[h] += pv[i];
+        }
+        // C fragment of S -> A fragment of P (keys 16 kk .. 16 kk + 15)
+        const int kk = nt >> 1, hi = nt & 1;
+        pa[kk][2 * hi] = pack_bf16(pv[0], pv[1]);
+        pa[kk][2 * hi + 1] = pack_bf16(pv[2], pv[3]);
+      }
+      // O += P V: V fragments (k = keys, n = dims) via ldmatrix.trans
+#pragma unroll
+      for (int kk = 0; kk < MMA_KEYS / 16; ++kk) {
+        if (c0 + kk * 16 >= len) break;
+        const uint32_t row_addr = lp::smem_u32(&Vs[kk * 16 + (lane & 15)][0]);
+#pragma unroll
+        for (int dt = 0; dt < DT; ++dt) {
+          uint32_t b0, b1;
+          asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                       : "=r"(b0), "=r"(b1)
+                       : "r"(row_addr + dt * 16));
+          mma_bf16_16816(o[dt], pa[kk], b0, b1);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!active) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float lsum = lrow[h];
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+    const int t = t0 + r0 + 8 * h;
+    if (t >= T) continue;
+    const float inv = 1.0f / lsum;
+    __nv_bfloat16* orow = out + ((int64_t)t * H + head) * HD + cq;
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt)
+      *reinterpret_cast<__nv_bfloat162*>(orow + dt * 8) =
+          __floats2bfloat162_rn(o[dt][2 * h] * inv, o[dt][2 * h + 1] * inv);
   }
 }
 
@@ -412,8 +647,23 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
   __nv_bfloat16* oo = (__nv_bfloat16*)out;
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 blk(ATT_WARPS * 32);
-  // many rows (prefill): a warp per row; few rows (decode): a CTA per row
-  const bool rpw = T * n_kv >= 1024;
+  // many rows (prefill): tensor-core row tiles (head_dim 64 / 128); few rows
+  // (decode): a CTA per row with warps splitting the keys
+  const bool many = T * n_kv >= 1024;
+  if (many && (head_dim == 64 || head_dim == 128)) {
+    const int G = n_heads / n_kv;
+    const dim3 mgrid((unsigned)((T + MMA_ROWS - 1) / MMA_ROWS), (unsigned)n_kv,
+                     (unsigned)((G + ATT_WARPS - 1) / ATT_WARPS));
+    const int Ti = (int)T;
+    if (head_dim == 64)
+      LP_CUDA(lp::launch(attention_mma_kernel<64>, mgrid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv,
+                         max_len, scale, oo));
+    else
+      LP_CUDA(lp::launch(attention_mma_kernel<128>, mgrid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv,
+                         max_len, scale, oo));
+    return 0;
+  }
+  const bool rpw = many;
   const dim3 grid(rpw ? (unsigned)((T + ATT_WARPS - 1) / ATT_WARPS) : (unsigned)T, (unsigned)n_kv);
   const int Ti = (int)T;
 #define LP_ATT(HDV)                                                                                              \

@@ -60,11 +60,14 @@ def test_gemm_swiglu_matches_fp32(n, k, t):
 
 @pytest.mark.parametrize("hd,H,KV,ctx,run", [(128, 32, 8, [1, 150, 37, 300], 40), (64, 4, 2, [5, 129, 64], 40),
                                               (128, 64, 8, [200, 17], 40), (128, 8, 8, [33, 96], 40),
-                                              (128, 64, 8, [300, 5], 200), (64, 4, 2, [600], 520)])
+                                              (128, 64, 8, [300, 5], 200), (64, 4, 2, [600], 520),
+                                              (128, 32, 8, [150, 100, 3], 150), (64, 16, 4, [300, 7], 299)])
 def test_attention_matches_fp32(hd, H, KV, ctx, run):
     """Ragged causal GQA attention (decode rows at arbitrary positions and a
     prefill-style run of ``run`` consecutive positions) vs a torch fp32
-    softmax; T x KV >= 1024 selects the warp-per-row (prefill) variant."""
+    softmax.  T x KV >= 1024 selects the prefill variants: smem-staged row
+    tiles when max_len's K/V fit (the last two cases; mixed-sequence tiles
+    read global memory), else a warp per row."""
     import torch
     g = torch.Generator(device="cuda").manual_seed(hd + H + len(ctx))
     seqs, max_len = len(ctx), max(ctx) + 8
