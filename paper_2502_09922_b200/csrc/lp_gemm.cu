@@ -802,6 +802,16 @@ int dispatch(const void* W, const void* W2, int64_t N, int64_t K, const void* X,
   if (T <= 32) return launch<32, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
   if (T <= 64) return launch<64, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
   if (T <= 128) return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  if constexpr (EPI == EPI_SWIGLU) {
+    // experiment switch: 128-token SwiGLU tiles (double-buffered TMEM, more
+    // tiles per wave) instead of 256 (single-buffered)
+    static int bt128 = -1;
+    if (bt128 < 0) {
+      const char* e = getenv("LP_SWIGLU_BT128");
+      bt128 = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (bt128) return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+  }
   return launch<256, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
 }
 

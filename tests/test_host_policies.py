@@ -1,0 +1,71 @@
+"""Host-side serving and kernel-launch policies (CPU only).
+
+* ``Server._admit``: FIFO admission into the active unit with the most free
+  slots — with the reference's one slot per unit (simengine.py:236,
+  ``batch_slots = 1``) this is exactly its unit-order fill
+  (simengine.py:356-368); with multi-slot replicas a burst is spread.
+* ``llama.gemm_split``: K splits for the residual-add GEMM (decode as
+  measured, prefill by wave efficiency over the 148-SM / 74-pair grid).
+"""
+from collections import deque
+
+from paper_2502_09922_b200 import llama as L
+from paper_2502_09922_b200.serving import Request, Server, Unit
+from paper_2502_09922_b200.workload import TraceRecord
+
+
+def _server(unit_slots):
+    srv = object.__new__(Server)          # admission needs only the unit table
+    srv.units = {i: Unit(i, "local", [], s, True, active=True) for i, s in enumerate(unit_slots)}
+    return srv
+
+
+def _queue(n):
+    return deque(Request(TraceRecord(f"r{i}", 0.001 * i, "m", 4, 2), [1, 2, 3, 4]) for i in range(n))
+
+
+def test_admission_single_slot_units_follow_unit_order():
+    srv = _server([1, 1, 1])
+    q = _queue(5)
+    srv._admit(q)
+    assert [srv.units[u].busy[0].rid for u in range(3)] == ["r0", "r1", "r2"]
+    assert [r.rid for r in q] == ["r3", "r4"]            # the rest wait, FIFO
+
+
+def test_admission_spreads_a_burst_over_replicas():
+    srv = _server([16, 16])
+    q = _queue(20)
+    srv._admit(q)
+    assert len(srv.units[0].busy) == 10 and len(srv.units[1].busy) == 10
+    assert not q
+    srv.units[0].retired = True                        # retired units take nothing
+    q = _queue(3)
+    srv._admit(q)
+    assert len(srv.units[0].busy) == 10 and len(srv.units[1].busy) == 13
+
+
+def test_admission_respects_capacity_and_inactive_units():
+    srv = _server([2, 2])
+    srv.units[1].active = False
+    q = _queue(5)
+    srv._admit(q)
+    assert len(srv.units[0].busy) == 2 and not srv.units[1].busy and len(q) == 3
+    for r in srv.units[0].busy.values():
+        assert r.unit == 0 and r.needs_prefill and r.kv_len == 0
+
+
+def test_gemm_split_policy():
+    # decode: ~160 CTAs of one wave (profiles/gemm_split_sweep_r01.txt), >= 4 k-blocks per split
+    assert L.gemm_split(6144, 4096, 16) == 3
+    assert L.gemm_split(4096, 14336, 1) == 5
+    assert L.gemm_split(32000, 256, 8) == 1
+    # prefill: QKV at T = 256 has 24 pair tiles for 74 cluster slots -> split
+    assert L.gemm_split(6144, 4096, 256) == 3
+    # >= 2 waves of tiles: never split (T = 4096, 8B shapes)
+    for n, k in ((6144, 4096), (4096, 4096), (4096, 14336)):
+        assert L.gemm_split(n, k, 4096) == 1
+    # every split keeps >= 8 k-blocks of 64
+    for n, k, t in ((1536, 512, 300), (640, 1024, 130), (10240, 8192, 256)):
+        s = L.gemm_split(n, k, t)
+        assert s == 1 or (k // 64) // s >= 8
+    assert L.gemm_token_tile(1) == 16 and L.gemm_token_tile(65) == 128 and L.gemm_token_tile(129) == 256
