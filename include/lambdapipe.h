@@ -170,13 +170,17 @@ int lp_gemm_bf16(const void* W, int64_t n_rows, int64_t k, const void* X, int64_
 int lp_gemm_swiglu(const void* W_gate, const void* W_up, int64_t n_rows, int64_t k, const void* X,
                    int64_t tokens, void* out_bf16, int64_t ldo, void* stream);
 int lp_embed(const void* table, int64_t d, const int32_t* tokens, int64_t T, float* x, void* stream);
+/* y_bf16[t,:] = x[t,:] * rsqrt(mean(x[t,:]^2) + eps) * w; d % 4 == 0 */
 int lp_rmsnorm(const float* x, const void* w, int64_t T, int64_t d, float eps, void* y, void* stream);
 /* RoPE (HF rotate_half) on q/k of qkv fp32 [T,(H+2KV)*hd]; q -> q_out bf16,
  * k/v appended to cache[seq][kv][pos][hd] bf16 */
 int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim, const int32_t* pos,
                const int32_t* seq, float theta, void* q_out, void* k_cache, void* v_cache, int64_t max_len,
                void* stream);
-/* ragged causal GQA attention: token t attends to 0..pos[t] of seq[t] */
+/* ragged causal GQA attention: token t attends to 0..pos[t] of seq[t].
+ * head_dim 32..128 (multiple of 32), H/KV <= 8.  T*KV >= 1024 (prefill):
+ * tensor-core tiles of 16 rows (mma.sync) when head_dim is 64 or 128 and the
+ * tile's rows share a sequence; otherwise CUDA-core online softmax. */
 int lp_attention(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
                  const int32_t* seq, int64_t T, int n_heads, int n_kv, int head_dim, int64_t max_len,
                  float scale, void* out, void* stream);
