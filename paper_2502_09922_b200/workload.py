@@ -158,3 +158,105 @@ def aggregate(events: list, label: str = "run", horizon_s: float | None = None) 
         rep.throughput_timeline.append((edge, (cursor - start) / THROUGHPUT_WINDOW_S))
     rep.gpu_seconds_cumulative = integrate_allocation(alloc, end)
     return rep
+
+
+# ---------------------------------------------------------------------------
+# Result files in the reference's layout (cli.py:218-281), so the reference's
+# ``blockcast report <outdir>`` (cli.py:413-432) re-aggregates a REAL run the
+# same way it aggregates a simulated one.
+
+def fmt(x) -> str:
+    """cli.py:218-223 number formatting."""
+    if x is None:
+        return ""
+    if isinstance(x, float):
+        return f"{x:.9g}"
+    return str(x)
+
+
+def event_lines(events: list) -> list:
+    """``events.log`` lines: ``time,kind,k=json;k=json`` (cli.py:231-238)."""
+    import json
+    out = []
+    for e in events:
+        payload = ";".join(f"{k}={json.dumps(v, sort_keys=True, separators=(',', ':'))}"
+                           for k, v in sorted(e.payload.items()))
+        out.append(f"{e.time_s:.9f},{e.kind},{payload}")
+    return out
+
+
+def parse_event_line(line: str) -> SimEvent:
+    """Inverse of :func:`event_lines` (cli.py:241-248)."""
+    import json
+    t, kind, payload = line.split(",", 2)
+    d = {}
+    if payload:
+        for item in payload.split(";"):
+            k, v = item.split("=", 1)
+            d[k] = json.loads(v)
+    return SimEvent(float(t), kind, d)
+
+
+def summary_block(r: MetricsReport) -> list:
+    """``summary.txt`` lines (cli.py:251-265)."""
+    return [
+        f"strategy: {r.label}",
+        f"requests_arrived: {r.requests_arrived}",
+        f"requests_completed: {r.requests_completed}",
+        f"requests_in_flight: {r.requests_in_flight}",
+        f"total_tokens: {r.total_tokens}",
+        f"ttft_p50_s: {fmt(r.ttft_p50)}",
+        f"ttft_p90_s: {fmt(r.ttft_p90)}",
+        f"ttft_p99_s: {fmt(r.ttft_p99)}",
+        f"first_token_s: {fmt(r.first_token_s)}",
+        f"time_to_first_served_s: {fmt(r.ramp_first_serve_s)}",
+        f"gpu_seconds_total: {fmt(r.gpu_seconds_cumulative)}",
+        f"end_s: {fmt(r.end_s)}",
+    ]
+
+
+def request_rows(events: list) -> list:
+    """(request_id, arrival_s, ttft_s, completion_s) per request in (arrival,
+    id) order — the reference builds them from its request table
+    (simengine.py:765-769); a real run derives the same from its events."""
+    arrival, first, done = {}, {}, {}
+    for e in events:
+        rid = e.payload.get("request")
+        if e.kind == "request_arrival":
+            arrival[rid] = e.time_s
+        elif e.kind == "token_emitted" and rid not in first:
+            first[rid] = e.time_s
+        elif e.kind == "request_done":
+            done[rid] = e.time_s
+    return [(rid, arrival[rid], None if rid not in first else first[rid] - arrival[rid], done.get(rid))
+            for rid in sorted(arrival, key=lambda r: (arrival[r], r))]
+
+
+def allocation_samples(events: list) -> list:
+    """(time, allocated GPUs) change points: (0, 0) then every ``allocation``
+    event (simengine.py:284, 295-298)."""
+    return [(0.0, 0)] + [(e.time_s, e.payload["allocated_gpus"]) for e in events if e.kind == "allocation"]
+
+
+def write_result(outdir, label: str, events: list, report: MetricsReport | None = None,
+                 horizon_s: float | None = None) -> None:
+    """Write ``<outdir>/<label>/{metrics_requests.csv, throughput.csv,
+    allocation.csv, events.log, summary.txt}`` exactly as cli.write_result
+    (cli.py:268-281) does for a simulated run."""
+    from pathlib import Path
+    d = Path(outdir) / label
+    d.mkdir(parents=True, exist_ok=True)
+    if report is None:
+        report = aggregate(events, label=label, horizon_s=horizon_s)
+
+    def write(name, lines):
+        (d / name).write_text("\n".join(lines) + ("\n" if lines else ""))
+
+    write("metrics_requests.csv", ["request_id,arrival_s,ttft_s,completion_s"] +
+          [f"{rid},{fmt(a)},{fmt(t)},{fmt(c)}" for rid, a, t, c in request_rows(events)])
+    write("throughput.csv", ["time_s,tokens_per_s"] +
+          [f"{fmt(t)},{fmt(v)}" for t, v in report.throughput_timeline])
+    write("allocation.csv", ["time_s,allocated_gpus"] +
+          [f"{fmt(t)},{v}" for t, v in allocation_samples(events)])
+    write("events.log", event_lines(events))
+    write("summary.txt", summary_block(report))

@@ -21,12 +21,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def run_burst(n_gpus: int, compress: float = 30.0, model: str = "llama2-7b", k: int = 2, blocks: int = 16,
-              local_slots: int = 16, limit_requests: int | None = None, seed: int = 4):
+              local_slots: int = 16, limit_requests: int | None = None, seed: int = 4, outdir: str | None = None):
     import numpy as np
 
     from paper_2502_09922_b200.autoscaler import AutoscaleServer
     from paper_2502_09922_b200.cluster import AutoscalePolicy
-    from paper_2502_09922_b200.workload import TraceRecord, aggregate, synth_burst
+    from paper_2502_09922_b200.workload import TraceRecord, aggregate, synth_burst, write_result
 
     raw = synth_burst(0.05, 6.0, [120.0, 800.0, 1500.0], 1800.0, seed=seed, spike_duration_s=60.0,
                       output_tokens=(16, 32))
@@ -46,6 +46,8 @@ def run_burst(n_gpus: int, compress: float = 30.0, model: str = "llama2-7b", k: 
         prompts = {r.request_id: rng.integers(0, vocab, r.prompt_tokens).tolist() for r in trace}
         ev = srv.run(trace, prompts)
         rep = aggregate(ev, "lambda_scale")
+        if outdir:   # the reference's result files: `blockcast report <outdir>` re-aggregates them
+            write_result(outdir, "lambda_scale", ev, rep)
         outs = sum(1 for e in ev if e.kind == "scale_out")
         busy = [x[1] for x in rep.throughput_timeline if x[1] > 0]
         return {"workload": f"{model} bf16, reference C5 trace ({len(trace)} requests) compressed {compress:g}x, "
@@ -65,5 +67,6 @@ if __name__ == "__main__":
     ap.add_argument("--gpus", type=int, default=4)
     ap.add_argument("--compress", type=float, default=30.0)
     ap.add_argument("--limit", type=int, default=0)
+    ap.add_argument("--outdir", default=None, help="write the reference's result files (cli.py:268-281) here")
     a = ap.parse_args()
-    print(json.dumps(run_burst(a.gpus, a.compress, limit_requests=a.limit or None)))
+    print(json.dumps(run_burst(a.gpus, a.compress, limit_requests=a.limit or None, outdir=a.outdir)))

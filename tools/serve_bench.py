@@ -19,14 +19,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int = 16, requests: int = 16,
                 prompt_len: int = 128, out_tokens: int = 32, spacing_s: float = 0.001, pull_ctas: int = 32,
-                local_slots: int = 16, seed: int = 20250815, executor: str = "ce"):
+                local_slots: int = 16, seed: int = 20250815, executor: str = "ce", outdir: str | None = None):
     import numpy as np
     import torch
 
     from paper_2502_09922_b200 import engine as E
     from paper_2502_09922_b200 import scaleout as SO
     from paper_2502_09922_b200.serving import Server
-    from paper_2502_09922_b200.workload import TraceRecord, aggregate
+    from paper_2502_09922_b200.workload import TraceRecord, aggregate, write_result
 
     plan = SO.plan_scale_out(model, n_gpus, k=k, block_count=blocks)
     lay = plan.layout
@@ -51,6 +51,8 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         srv2 = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs)
         ev = srv2.run(trace, prompts, streams, pull_ctas=pull_ctas, executor=executor)
         rep = aggregate(ev, "lambda_scale")
+        if outdir:   # the reference's result files: `blockcast report <outdir>` re-aggregates them
+            write_result(outdir, "lambda_scale", ev, rep)
         first_full = min(srv2.block_complete_s.values()) if srv2.block_complete_s else None
         all_full = max(srv2.block_complete_s.values()) if srv2.block_complete_s else None
         t_switch = next((e.time_s for e in ev if e.kind == "mode_switch"), None)
@@ -104,6 +106,7 @@ if __name__ == "__main__":
     ap.add_argument("--out-tokens", type=int, default=32)
     ap.add_argument("--executor", default="ce")
     ap.add_argument("--pull-ctas", type=int, default=32)
+    ap.add_argument("--outdir", default=None, help="write the reference's result files (cli.py:268-281) here")
     a = ap.parse_args()
     print(json.dumps(run_serving(a.gpus, a.model, a.k, a.blocks, a.requests, out_tokens=a.out_tokens,
-                                 executor=a.executor, pull_ctas=a.pull_ctas)))
+                                 executor=a.executor, pull_ctas=a.pull_ctas, outdir=a.outdir)))
