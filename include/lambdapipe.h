@@ -132,6 +132,12 @@ int lp_mc_run_ce(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const
  * with the GPU->GPU relay. */
 int lp_mc_run_host_dma(lp_mc* mc, int node, uint32_t epoch, int n_streams, void* const* streams,
                        void* const* block_events);
+/* Landing events without touching peer memory: on `stream` (a stream of
+ * `node`'s device), for every block `node` receives this epoch, wait until
+ * its OWN block counter is complete (cuStreamWaitValue32 on local memory)
+ * and record block_events[block] (created on that device).  Lets a caller
+ * time per-block arrivals whichever executor/direction delivers them. */
+int lp_mc_landing_events(lp_mc* mc, int node, uint32_t epoch, void* stream, void* const* block_events);
 /* Verify-as-it-lands: zero sums_dev[n_blocks] (device memory) and launch
  * `ctas` CTAs on `stream` that checksum every block `node` receives this
  * epoch, tile by tile as its flags publish (either executor), with the

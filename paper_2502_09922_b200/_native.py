@@ -57,6 +57,7 @@ SIGNATURES = {
     "lp_mc_status": [_vp, _vp, _P(C.c_int)],
     "lp_mc_configure": [_vp, C.c_int, C.c_int, C.c_int, _i64, C.c_int],
     "lp_mc_run_ce": [_vp, C.c_int, _u32, C.c_int, _P(_vp), _P(_vp)],
+    "lp_mc_landing_events": [_vp, C.c_int, _u32, _vp, _P(_vp)],
     "lp_mc_run_host_dma": [_vp, C.c_int, _u32, C.c_int, _P(_vp), _P(_vp)],
     "lp_mc_node_ops": [_vp, C.c_int, _P(C.c_int), _P(C.c_int)],
     "lp_mc_verify": [_vp, C.c_int, _u32, C.c_int, _vp, _vp],

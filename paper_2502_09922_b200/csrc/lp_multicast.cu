@@ -900,6 +900,26 @@ int lp_mc_run_host_dma(lp_mc* mc, int node, uint32_t epoch, int n_streams, void*
   return enqueue_ce(mc, node, epoch, seq, n_streams, streams, block_events);
 }
 
+int lp_mc_landing_events(lp_mc* mc, int node, uint32_t epoch, void* stream, void* const* block_events) {
+  if (resolve_stream_memops() != 0) return -1;
+  LP_CHECK(mc && node >= 0 && node < mc->n_nodes && block_events && epoch >= 1,
+           "lp_mc_landing_events: bad arguments");
+  LP_CHECK(mc->nodes[node].kind == LP_NODE_GPU && mc->nodes[node].counts,
+           "lp_mc_landing_events: node %d is not a GPU node with signals", node);
+  if (mc->dirty && compile(mc) != 0) return -2;
+  std::vector<char> recv(mc->n_blocks, 0);
+  for (const OpDev& op : mc->h_ops)
+    if (op.dst == node) recv[op.block] = 1;
+  for (int b = 0; b < mc->n_blocks; ++b) {
+    if (!recv[b] || !block_events[b]) continue;
+    CUresult r = cuStreamWaitValue32((CUstream)stream, (CUdeviceptr)(mc->nodes[node].counts + b),
+                                     epoch * (uint32_t)mc->blocks[b].ntiles, CU_STREAM_WAIT_VALUE_GEQ);
+    LP_CHECK(r == CUDA_SUCCESS, "lp_mc_landing_events: cuStreamWaitValue32 failed (%d)", (int)r);
+    LP_CUDA(cudaEventRecord((cudaEvent_t)block_events[b], (cudaStream_t)stream));
+  }
+  return 0;
+}
+
 // Ops the kernel (push + pull roles) and the host DMA would execute for node.
 int lp_mc_node_ops(lp_mc* mc, int node, int* kernel_ops, int* dma_ops) {
   LP_CHECK(mc && node >= 0 && node < mc->n_nodes && kernel_ops && dma_ops, "lp_mc_node_ops: bad arguments");

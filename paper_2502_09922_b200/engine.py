@@ -99,6 +99,7 @@ class MulticastEngine:
         """direction 0 = senders push, 1 = receivers pull; copy engine per role:
         0 = LDG/STG vectors, 1 = TMA bulk pipeline; window = ops an LDG CTA may interleave."""
         N.call("lp_mc_configure", self._h, direction, push_mode, pull_mode, chunk_bytes, window)
+        self.cfg = (direction, push_mode, pull_mode, chunk_bytes, window)
 
     def set_option(self, name: str, value: int):
         N.call("lp_mc_set_option", self._h, name.encode(), int(value))
@@ -126,6 +127,12 @@ class MulticastEngine:
         if block_events is not None:
             evs = (C.c_void_p * self.n_blocks)(*[int(e) if e else None for e in block_events])
         N.call("lp_mc_run_host_dma", self._h, node, epoch, len(streams), arr, evs)
+
+    def landing_events(self, node: int, epoch: int, stream: int, block_events: list):
+        """Record block_events[b] on ``stream`` once ``node`` holds block b
+        (waits on the node's own counters; see lp_mc_landing_events)."""
+        evs = (C.c_void_p * self.n_blocks)(*[int(e) if e else None for e in block_events])
+        N.call("lp_mc_landing_events", self._h, node, epoch, C.c_void_p(stream), evs)
 
     def verify(self, node: int, epoch: int, sums_ptr: int, stream: int = 0, ctas: int = 32):
         """Checksum ``node``'s received blocks as they land (lp_mc_verify)
@@ -410,11 +417,22 @@ class Cluster:
 
     def launch_devices_ce(self, streams: dict) -> int:
         """Multi-device launch on copy engines: every GPU node's ops enqueued
-        on its device's stream (``streams``: device -> torch stream)."""
+        on its device's stream (``streams``: device -> torch stream).
+
+        Always in the PUSH direction (senders' copy engines write into the
+        receivers, waits on the sender's OWN flags): with one process owning
+        every GPU, a stream waiting (cuStreamWaitValue32) on another device's
+        native allocation deadlocks once relays wait on each other across
+        devices — GPU0 -> 3 peers hung in the pull direction and completes in
+        push (tools/relay_check.py; one process per GPU, whose peers' flags
+        are IPC mappings, pulls fine)."""
         self.epoch += 1
         self._mc_streams = {}
         for d, eng in self.per_device.items():
             N.call("lp_set_device", d)
+            cfg = getattr(eng, "cfg", (1, 0, 0, 16384, 3))
+            if cfg[0] != 0:
+                eng.configure(0, *cfg[1:])
             st = streams[d]
             ptr = st if isinstance(st, int) else st.cuda_stream
             for nb in self.nodes:

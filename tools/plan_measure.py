@@ -8,8 +8,9 @@ Writes what the reference's ``cmd_plan`` writes (cli.py:288-339) —
 ``summary.txt`` with the reference's modelled lines (cluster = one 8×B200
 box: NVLink 900 GB/s as the fabric, ``cluster.b200_box``) — and appends the
 MEASURED counterparts: the schedule executed on the copy engines of N GPUs
-(one process, ``engine.Cluster.devices``), a CUDA event recorded on each
-receiver's stream as each block lands (``lp_mc_run_ce`` block events):
+(one process, ``engine.Cluster.devices``, push direction), a CUDA event
+recorded on each receiver's side stream as each block lands
+(``lp_mc_landing_events``: waits on the receiver's own block counters):
 transfer time, per-node completion, per-step time and the first pipeline's
 activation (its stages' blocks landed).  ``--sweep-b`` adds ``sweep.csv``
 in the reference's sweep layout (cli.py:372-410) with the measured columns
@@ -47,10 +48,8 @@ def measure(model: str, n: int, k: int, b: int, reps: int = 3, seed: int = 5):
         for s in plan.sources:
             E.load_source_image(cl, s, lay, seed)
         cl.set_schedule_all(plan.schedule, plan.sources)
-        for d in range(n):
-            N.call("lp_set_device", d)
-            cl.per_device[d].configure(1, 0, 0, 16384, 3)      # receivers pull
-        streams = {d: torch.cuda.Stream(device=d) for d in range(n)}
+        streams = {d: torch.cuda.Stream(device=d) for d in range(n)}       # copy-engine ops
+        ev_streams = {d: torch.cuda.Stream(device=d) for d in range(n)}    # landing events
 
         def event(dev):
             N.call("lp_set_device", dev)
@@ -66,15 +65,15 @@ def measure(model: str, n: int, k: int, b: int, reps: int = 3, seed: int = 5):
         for rep in range(reps + 1):
             for d in range(n):
                 torch.cuda.synchronize(d)
-            cl.epoch += 1
             for node in recv:
                 d = dev_of[node]
                 N.call("lp_set_device", d)
-                N.call("lp_event_record", C.c_void_p(start[node]), C.c_void_p(streams[d].cuda_stream))
+                N.call("lp_event_record", C.c_void_p(start[node]), C.c_void_p(ev_streams[d].cuda_stream))
+            epoch = cl.launch_devices_ce(streams)          # push direction (see launch_devices_ce)
             for node in recv:
                 d = dev_of[node]
                 N.call("lp_set_device", d)
-                cl.per_device[d].run_ce(node, cl.epoch, [streams[d].cuda_stream], block_events=blk_ev[node])
+                cl.per_device[d].landing_events(node, epoch, ev_streams[d].cuda_stream, blk_ev[node])
             arr = {}
             for node in recv:
                 ms = C.c_float()
@@ -136,7 +135,7 @@ def write_plan(outdir: Path, model: str, k: int, m: dict):
     for node, step in schedule_summary(sched)["completion_step"].items():
         out.append(f"completion_step node {node}: {step}")
     out += [
-        "measured_executor: copy engines (256 MiB tiles), one process driving the GPUs, byte-exact",
+        "measured_executor: copy engines, push direction (256 MiB tiles), one process driving the GPUs, byte-exact",
         f"measured_transfer_s: {_fmt(m['transfer_s'])}",
         f"measured_step_time_s: {_fmt(m['transfer_s'] / sched.step_count)}",
         f"measured_first_pipeline_activation_s: {_fmt(m['first_activation_s'])}",
