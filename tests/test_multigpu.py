@@ -26,3 +26,18 @@ def test_distributed_multicast_all_executors():
     assert res.returncode == 0 and line, res.stdout[-2000:] + res.stderr[-2000:]
     out = json.loads(line[-1])
     assert out["ok"] and len(out["results"]) == 5, out
+
+
+@pytest.mark.skipif(gpu_count() < 3, reason="needs >= 3 GPUs for cross-device relays")
+@pytest.mark.parametrize("executor", ["ce", "kernel"])
+def test_single_process_relays(executor):
+    """One process driving several GPUs (as serving and the autoscaler do)
+    through a schedule whose relays wait on each other across devices: the
+    copy-engine executor must not deadlock (it runs in the push direction in
+    this mode) and every receiver ends byte-exact.  Run in a subprocess with
+    a timeout, since a stream-level deadlock has no watchdog."""
+    n = min(gpu_count(), 4)
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "relay_check.py"), str(n), "1", "4", executor],
+                         capture_output=True, text=True, timeout=150, cwd=ROOT, env=env)
+    assert res.returncode == 0 and "byte-exact" in res.stdout, res.stdout[-2000:] + res.stderr[-2000:]

@@ -76,7 +76,7 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
             for row in srv2.profile:
                 print("iter t=%.4f enq=%.4f dev=%.4f tokens=%d batches=%d" % row, file=sys.stderr)
         return {
-            "multicast_executor": executor,
+            "multicast_executor": executor + (" (push direction: one process drives every GPU, DESIGN §5.1)" if executor == "ce" else ""),
             "workload": f"{model} bf16, GPU sources {plan.sources}, receivers {plan.receivers}, b={blocks}, k={k}; "
                         f"{requests} requests x (prompt {prompt_len}, out {out_tokens}), {spacing_s * 1e3:.0f} ms apart at t=0",
             "pipelines": [[(st.node, st.block_lo, st.block_hi) for st in ep.stages] for ep in plan.pipelines],
