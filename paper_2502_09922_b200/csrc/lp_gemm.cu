@@ -521,7 +521,11 @@ struct Cfg2 {
   static constexpr int NBUF = 2 * ACC_COLS <= 512 ? 2 : 1;
   static constexpr int TC = NBUF * ACC_COLS;
   static constexpr int TCOLS = TC <= 32 ? 32 : TC <= 64 ? 64 : TC <= 128 ? 128 : TC <= 256 ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;
+  // SwiGLU epilogue transpose tiles: per epilogue warp 32 tokens x 32 rows
+  // bf16, rows padded to 80 B (conflict-free 16-byte reads)
+  static constexpr int XPOSE_PITCH = 40;                      // bf16 elements per token row
+  static constexpr int XPOSE_BYTES = (EPI == EPI_SWIGLU) ? 4 * 32 * XPOSE_PITCH * 2 : 0;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + XPOSE_BYTES;
 };
 
 template <int BT, int EPI>
@@ -653,7 +657,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (CH == 32) tmem_ld32(taddr + BT, u); else tmem_ld16(taddr + BT, u);
         }
         tmem_wait_ld();
-        if (n < args.n_rows) {
+        if constexpr (EPI == EPI_SWIGLU && CH == 32) {
+          // transpose through smem so each lane stores one token's 32
+          // consecutive outputs as 4 x 16 B (a warp writes whole 128 B lines
+          // instead of 64 B per token) — the SwiGLU tile is single-buffered,
+          // so its epilogue is on the critical path
+          __nv_bfloat16* xt = reinterpret_cast<__nv_bfloat16*>(smem + C::STAGES * C::STAGE_BYTES) +
+                              (size_t)quarter * 32 * C::XPOSE_PITCH;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = __uint_as_float(v[j]), up = __uint_as_float(u[j]);
+            xt[j * C::XPOSE_PITCH + lane] = __float2bfloat16_rn(x / (1.0f + __expf(-x)) * up);
+          }
+          __syncwarp();
+          const int t = t0 + c + lane;
+          const int nb = n0 + quarter * 32;                        // this warp's first row
+          if (t < args.tokens) {
+            __nv_bfloat16* orow = (__nv_bfloat16*)args.out + (int64_t)t * args.ldo + nb;
+            const int4* src = reinterpret_cast<const int4*>(xt + lane * C::XPOSE_PITCH);
+            if (nb + 32 <= args.n_rows && ((((uintptr_t)orow) & 15) == 0)) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) reinterpret_cast<int4*>(orow)[q] = src[q];
+            } else {
+              for (int r = 0; r < 32 && nb + r < args.n_rows; ++r) orow[r] = xt[lane * C::XPOSE_PITCH + r];
+            }
+          }
+          __syncwarp();                                            // xt is rewritten for the next chunk
+        } else if (n < args.n_rows) {
 #pragma unroll
           for (int j = 0; j < CH; ++j) {
             const int t = t0 + c + j;
