@@ -178,6 +178,10 @@ int lp_gemm_swiglu(const void* W_gate, const void* W_up, int64_t n_rows, int64_t
 int lp_embed(const void* table, int64_t d, const int32_t* tokens, int64_t T, float* x, void* stream);
 /* y_bf16[t,:] = x[t,:] * rsqrt(mean(x[t,:]^2) + eps) * w; d % 4 == 0 */
 int lp_rmsnorm(const float* x, const void* w, int64_t T, int64_t d, float eps, void* y, void* stream);
+/* lp_rmsnorm that also zeroes the fp32 [T, zero_cols] buffer `zero` (the
+ * next split-K GEMM's accumulator) in the same launch */
+int lp_rmsnorm_zero(const float* x, const void* w, int64_t T, int64_t d, float eps, void* y, float* zero,
+                    int64_t zero_cols, void* stream);
 /* RoPE (HF rotate_half) on q/k of qkv fp32 [T,(H+2KV)*hd]; q -> q_out bf16,
  * k/v appended to cache[seq][kv][pos][hd] bf16 */
 int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim, const int32_t* pos,

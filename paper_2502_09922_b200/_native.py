@@ -69,6 +69,7 @@ SIGNATURES = {
     "lp_gemm_swiglu": [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
     "lp_embed": [_vp, _i64, _vp, _i64, _vp, _vp],
     "lp_rmsnorm": [_vp, _vp, _i64, _i64, C.c_float, _vp, _vp],
+    "lp_rmsnorm_zero": [_vp, _vp, _i64, _i64, C.c_float, _vp, _vp, _i64, _vp],
     "lp_rope_kv": [_vp, _i64, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_float, _vp, _vp, _vp, _i64, _vp],
     "lp_attention": [_vp, _vp, _vp, _vp, _vp, _i64, C.c_int, C.c_int, C.c_int, _i64, C.c_float, _vp, _vp],
     "lp_argmax": [_vp, _i64, _i64, _vp, _vp, _vp],

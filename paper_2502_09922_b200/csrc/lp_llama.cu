@@ -37,12 +37,27 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ table, int64_t d,
 // (one HBM read of x instead of two: prefill rows are 16-32 KB).
 constexpr int RMS_THREADS = 512;
 constexpr int RMS_CACHE = 4;     // float4 per thread held in registers (d <= 8192)
+//
+// zero (optional): also clear row t of an fp32 [T, zero_cols] buffer — the
+// accumulator the next (split-K, red.add) GEMM adds into — so no separate
+// fill kernel sits between the norm and the GEMM (a non-PDL fill would also
+// break the programmatic-launch chain inside captured graphs).
 __global__ void __launch_bounds__(RMS_THREADS) rmsnorm_kernel(const float* __restrict__ x,
                                                               const __nv_bfloat16* __restrict__ w, int64_t d,
-                                                              float eps, __nv_bfloat16* __restrict__ y) {
+                                                              float eps, __nv_bfloat16* __restrict__ y,
+                                                              float* __restrict__ zero, int64_t zero_cols) {
   lp::pdl_wait();
   lp::pdl_trigger();
   const int t = blockIdx.x;
+  if (zero) {
+    float* zr = zero + (int64_t)t * zero_cols;
+    if ((zero_cols & 3) == 0 && (((uintptr_t)zr) & 15) == 0) {
+      for (int64_t i = threadIdx.x; i < zero_cols / 4; i += RMS_THREADS)
+        reinterpret_cast<float4*>(zr)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      for (int64_t i = threadIdx.x; i < zero_cols; i += RMS_THREADS) zr[i] = 0.f;
+    }
+  }
   const int n4 = (int)(d / 4);
   const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)t * d);
   const uint2* wr = reinterpret_cast<const uint2*>(w);
@@ -90,12 +105,14 @@ __global__ void __launch_bounds__(RMS_THREADS) rmsnorm_kernel(const float* __res
 // pairs with j + hd/2 at angle pos * theta^(-2j/hd).
 // q_out [T, H*hd] bf16; k/v appended to cache[seq][kv][pos][hd] bf16.
 //
-// One CTA per token: the angle table (cos, sin of pos * theta^(-2j/hd), j < hd/2)
-// depends only on the token's position, so it is computed once into smem and
-// shared by all H + KV rotated heads (a CTA per (token, head) recomputed it
-// per head: 87 us per 70B prefill layer at T = 1024); v heads are copied.
+// One CTA per (token, group of 8 heads): the angle table (cos, sin of
+// pos * theta^(-2j/hd), j < hd/2) depends only on the token's position, so it
+// is computed once into smem and shared by the group's rotated heads (a CTA
+// per (token, head) recomputed it per head: 87 us per 70B prefill layer at
+// T = 1024); one more CTA per token copies the v heads.
 constexpr int ROPE_THREADS = 256;
 constexpr int ROPE_MAX_HALF = 128;
+constexpr int ROPE_HEADS = 8;      // rotated heads per CTA
 __global__ void __launch_bounds__(ROPE_THREADS) rope_kv_kernel(
     const float* __restrict__ qkv, int H, int KV, int hd, const int32_t* __restrict__ pos,
     const int32_t* __restrict__ seq, float theta, __nv_bfloat16* __restrict__ q_out,
@@ -116,21 +133,28 @@ __global__ void __launch_bounds__(ROPE_THREADS) rope_kv_kernel(
     s_sin[j] = sn;
   }
   __syncthreads();
+  // grid.y splits the token's heads over CTAs (decode has only a handful of
+  // tokens): y < groups rotates ROPE_HEADS q/k heads, y == groups copies v
   const float* row = qkv + (int64_t)t * (H + 2 * KV) * hd;
-  const int rot = (H + KV) * half;                       // rotated (q and k) pairs
-  for (int i = threadIdx.x; i < rot; i += blockDim.x) {
-    const int head = i / half, j = i % half;
-    const float* src = row + (int64_t)head * hd;
-    __nv_bfloat16* dst = head < H ? q_out + ((int64_t)t * H + head) * hd
-                                  : k_cache + (((int64_t)sq * KV + (head - H)) * max_len + p) * hd;
-    const float a = src[j], b = src[j + half], cs = s_cos[j], sn = s_sin[j];
-    dst[j] = __float2bfloat16_rn(a * cs - b * sn);
-    dst[j + half] = __float2bfloat16_rn(b * cs + a * sn);
-  }
-  const float* vsrc = row + (int64_t)(H + KV) * hd;
-  for (int i = threadIdx.x; i < KV * hd; i += blockDim.x) {
-    const int kh = i / hd, j = i % hd;
-    v_cache[(((int64_t)sq * KV + kh) * max_len + p) * hd + j] = __float2bfloat16_rn(vsrc[i]);
+  const int groups = (H + KV + ROPE_HEADS - 1) / ROPE_HEADS;
+  if ((int)blockIdx.y < groups) {
+    const int h0 = blockIdx.y * ROPE_HEADS;
+    const int h1 = min(H + KV, h0 + ROPE_HEADS);
+    for (int i = threadIdx.x; i < (h1 - h0) * half; i += blockDim.x) {
+      const int head = h0 + i / half, j = i % half;
+      const float* src = row + (int64_t)head * hd;
+      __nv_bfloat16* dst = head < H ? q_out + ((int64_t)t * H + head) * hd
+                                    : k_cache + (((int64_t)sq * KV + (head - H)) * max_len + p) * hd;
+      const float a = src[j], b = src[j + half], cs = s_cos[j], sn = s_sin[j];
+      dst[j] = __float2bfloat16_rn(a * cs - b * sn);
+      dst[j + half] = __float2bfloat16_rn(b * cs + a * sn);
+    }
+  } else {
+    const float* vsrc = row + (int64_t)(H + KV) * hd;
+    for (int i = threadIdx.x; i < KV * hd; i += blockDim.x) {
+      const int kh = i / hd, j = i % hd;
+      v_cache[(((int64_t)sq * KV + kh) * max_len + p) * hd + j] = __float2bfloat16_rn(vsrc[i]);
+    }
   }
 }
 
@@ -648,10 +672,16 @@ int lp_embed(const void* table, int64_t d, const int32_t* tokens, int64_t T, flo
 }
 
 int lp_rmsnorm(const float* x, const void* w, int64_t T, int64_t d, float eps, void* y, void* stream) {
+  return lp_rmsnorm_zero(x, w, T, d, eps, y, nullptr, 0, stream);
+}
+
+int lp_rmsnorm_zero(const float* x, const void* w, int64_t T, int64_t d, float eps, void* y, float* zero,
+                    int64_t zero_cols, void* stream) {
   LP_CHECK(x && w && y && T > 0 && d > 0, "lp_rmsnorm: bad arguments");
   LP_CHECK(d % 4 == 0, "lp_rmsnorm: d must be a multiple of 4");
+  LP_CHECK(!zero || zero_cols > 0, "lp_rmsnorm_zero: zero_cols must be positive");
   LP_CUDA(lp::launch(rmsnorm_kernel, dim3((unsigned)T), dim3(RMS_THREADS), 0, (cudaStream_t)stream, x,
-                     (const __nv_bfloat16*)w, d, eps, (__nv_bfloat16*)y));
+                     (const __nv_bfloat16*)w, d, eps, (__nv_bfloat16*)y, zero, zero_cols));
   return 0;
 }
 
@@ -661,7 +691,8 @@ int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim,
   LP_CHECK(qkv && pos && seq && q_out && k_cache && v_cache && T > 0, "lp_rope_kv: bad arguments");
   LP_CHECK(n_kv > 0 && n_heads % n_kv == 0 && head_dim % 2 == 0, "lp_rope_kv: bad head shape");
   LP_CHECK(head_dim / 2 <= ROPE_MAX_HALF, "lp_rope_kv: head_dim > %d", 2 * ROPE_MAX_HALF);
-  LP_CUDA(lp::launch(rope_kv_kernel, dim3((unsigned)T), dim3(ROPE_THREADS), 0, (cudaStream_t)stream, qkv, n_heads, n_kv,
+  const unsigned groups = (unsigned)((n_heads + n_kv + ROPE_HEADS - 1) / ROPE_HEADS);
+  LP_CUDA(lp::launch(rope_kv_kernel, dim3((unsigned)T, groups + 1), dim3(ROPE_THREADS), 0, (cudaStream_t)stream, qkv, n_heads, n_kv,
                      head_dim, pos, seq, theta, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
                      (__nv_bfloat16*)v_cache, max_len));
   return 0;

@@ -171,10 +171,10 @@ class LlamaExecutor:
         s = C.c_void_p(stream)
         dev = self.torch_device
         h = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
-        N.check(self.lib.lp_rmsnorm(_vp(x), C.c_void_p(self.ptr(f"layers.{l}.attn_norm")), T, d, cfg.norm_eps,
-                                    _vp(h), s), "lp_rmsnorm")
         nq = (H + 2 * KV) * hd
-        qkv = torch.zeros((T, nq), dtype=torch.float32, device=dev)
+        qkv = torch.empty((T, nq), dtype=torch.float32, device=dev)    # zeroed by the norm kernel
+        N.check(self.lib.lp_rmsnorm_zero(_vp(x), C.c_void_p(self.ptr(f"layers.{l}.attn_norm")), T, d, cfg.norm_eps,
+                                         _vp(h), _vp(qkv), nq, s), "lp_rmsnorm_zero")
         self._gemm_add(self.ptr(f"layers.{l}.wq"), nq, d, h, T, qkv, nq, stream)
         q = torch.empty((T, H * hd), dtype=torch.bfloat16, device=dev)
         N.check(self.lib.lp_rope_kv(_vp(qkv), T, H, KV, hd, _vp(pos), _vp(seq), cfg.rope_theta, _vp(q),
