@@ -434,10 +434,11 @@ class Cluster:
             if cfg[0] != 0:
                 eng.configure(0, *cfg[1:])
             st = streams[d]
-            ptr = st if isinstance(st, int) else st.cuda_stream
+            sts = list(st) if isinstance(st, (list, tuple)) else [st]     # several: ops round-robin
+            ptrs = [x if isinstance(x, int) else x.cuda_stream for x in sts]
             for nb in self.nodes:
                 if nb.kind == LP_NODE_GPU and nb.device == d:
-                    eng.run_ce(nb.node, self.epoch, [ptr])
+                    eng.run_ce(nb.node, self.epoch, ptrs)
         return self.epoch
 
     def wait_devices(self) -> None:

@@ -33,7 +33,7 @@ def _fmt(x):
     return fmt(x)
 
 
-def measure(model: str, n: int, k: int, b: int, reps: int = 3, seed: int = 5):
+def measure(model: str, n: int, k: int, b: int, reps: int = 3, seed: int = 5, ce_streams: int = 1):
     import torch
 
     from paper_2502_09922_b200 import _native as N
@@ -48,7 +48,7 @@ def measure(model: str, n: int, k: int, b: int, reps: int = 3, seed: int = 5):
         for s in plan.sources:
             E.load_source_image(cl, s, lay, seed)
         cl.set_schedule_all(plan.schedule, plan.sources)
-        streams = {d: torch.cuda.Stream(device=d) for d in range(n)}       # copy-engine ops
+        streams = {d: [torch.cuda.Stream(device=d) for _ in range(ce_streams)] for d in range(n)}  # CE ops
         ev_streams = {d: torch.cuda.Stream(device=d) for d in range(n)}    # landing events
 
         def event(dev):
@@ -155,11 +155,12 @@ if __name__ == "__main__":
     ap.add_argument("--b", type=int, default=16)
     ap.add_argument("--sweep-b", default="")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--ce-streams", type=int, default=1, help="copy-engine streams per GPU (ops round-robin)")
     ap.add_argument("--outdir", default="gpurun_out/plan_measure")
     a = ap.parse_args()
     out = Path(a.outdir)
     if not a.sweep_b:
-        print("\n".join(write_plan(out, a.model, a.k, measure(a.model, a.gpus, a.k, a.b, a.reps))))
+        print("\n".join(write_plan(out, a.model, a.k, measure(a.model, a.gpus, a.k, a.b, a.reps, ce_streams=a.ce_streams))))
     else:
         from paper_2502_09922_b200.cluster import b200_box
         from paper_2502_09922_b200.image import CONFIGS, model_spec
@@ -171,7 +172,7 @@ if __name__ == "__main__":
                 "measured_first_pipeline_activation_s,measured_nvlink_roofline_frac"]
         for raw in a.sweep_b.split(","):
             b = int(raw)
-            m = measure(a.model, a.gpus, a.k, b, a.reps)
+            m = measure(a.model, a.gpus, a.k, b, a.reps, ce_streams=a.ce_streams)
             write_plan(out / f"b_{b}", a.model, a.k, m)
             size = m["plan"].layout.weights_bytes
             rows.append(f"b,{b},{elbow},{_fmt(predicted_transfer_s(size, b, a.gpus, cl.step_fixed_overhead_s, cl.nic_Bps))},"
