@@ -571,6 +571,176 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
   }
 }
 
+// Decode on the tensor cores: one CTA per (token, kv head).  The G query
+// heads of the GQA group share the token's K/V, so they form the rows of an
+// m16n8k16 tile (rows >= G are zero); each warp takes 32-key chunks
+// (warp w: keys 32w, 32w + 128, ...), stages them in its own padded smem
+// slice, runs S = QKᵀ, online softmax and PV on the tensor cores, and the
+// four warps merge (m, l, O) through smem at the end.  The CUDA-core
+// lane-per-key loop took 28.7 us per 8B layer at B = 16, ctx 160
+// (tools/attn_perf.py): a chain of dependent loads per 32 keys.
+constexpr int DEC_KEYS = 32;
+
+template <int HD>
+__global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
+    const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
+    const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
+    int H, int KV, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
+  constexpr int KS = HD + 8;
+  constexpr int KSTEPS = HD / 16;
+  constexpr int DT = HD / 8;
+  extern __shared__ __align__(16) uint8_t dec_smem[];
+  __shared__ float sm_m[ATT_WARPS][16], sm_l[ATT_WARPS][16];
+  lp::pdl_wait();
+  lp::pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x, kh = blockIdx.y;
+  const int G = H / KV;
+  const int L = pos[t] + 1;
+  const int r0 = lane >> 2, cq = (lane & 3) * 2;
+  const __nv_bfloat16* kg = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+  const __nv_bfloat16* vg = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+  __nv_bfloat16 (*Kw)[KS] = reinterpret_cast<__nv_bfloat16 (*)[KS]>(dec_smem) + warp * 2 * DEC_KEYS;
+  __nv_bfloat16 (*Vw)[KS] = Kw + DEC_KEYS;
+  uint32_t qa[KSTEPS][4];
+#pragma unroll
+  for (int ks = 0; ks < KSTEPS; ++ks) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = r0 + 8 * h;
+      const __nv_bfloat16* qr = q + ((int64_t)t * H + kh * G + (row < G ? row : 0)) * HD + ks * 16 + cq;
+      qa[ks][h] = row < G ? *reinterpret_cast<const uint32_t*>(qr) : 0u;
+      qa[ks][2 + h] = row < G ? *reinterpret_cast<const uint32_t*>(qr + 8) : 0u;
+    }
+  }
+  float o[DT][4];
+#pragma unroll
+  for (int i = 0; i < DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const float sl2 = scale * 1.4426950408889634f;
+  for (int c0 = warp * DEC_KEYS; c0 < L; c0 += ATT_WARPS * DEC_KEYS) {
+    const int nk = min(DEC_KEYS, L - c0);
+    {   // lane j stages key c0 + j (zero past the context)
+      const int4* kr = reinterpret_cast<const int4*>(kg + (int64_t)(c0 + lane) * HD);
+      const int4* vr = reinterpret_cast<const int4*>(vg + (int64_t)(c0 + lane) * HD);
+      int4 kv[HD / 8], vv[HD / 8];
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        kv[i] = lane < nk ? kr[i] : make_int4(0, 0, 0, 0);
+        vv[i] = lane < nk ? vr[i] : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        reinterpret_cast<int4*>(&Kw[lane][0])[i] = kv[i];
+        reinterpret_cast<int4*>(&Vw[lane][0])[i] = vv[i];
+      }
+    }
+    __syncwarp();
+    float sc[DEC_KEYS / 8][4];
+#pragma unroll
+    for (int nt = 0; nt < DEC_KEYS / 8; ++nt) {
+      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+      const __nv_bfloat16* kr = &Kw[nt * 8 + r0][cq];
+#pragma unroll
+      for (int ks = 0; ks < KSTEPS; ++ks) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + ks * 16);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(kr + ks * 16 + 8);
+        mma_bf16_16816(sc[nt], qa[ks], b0, b1);
+      }
+    }
+    float mnew[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < DEC_KEYS / 8; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = c0 + nt * 8 + cq + e;
+          float v = sc[nt][2 * h + e] * sl2;
+          if (key >= L) v = -INFINITY;
+          sc[nt][2 * h + e] = v;
+          mx = fmaxf(mx, v);
+        }
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      mnew[h] = fmaxf(mrow[h], mx);
+      const float corr = mnew[h] == -INFINITY ? 1.f : exp2f(mrow[h] - mnew[h]);
+      lrow[h] *= corr;
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) {
+        o[dt][2 * h] *= corr;
+        o[dt][2 * h + 1] *= corr;
+      }
+      mrow[h] = mnew[h];
+    }
+    uint32_t pa[DEC_KEYS / 16][4];
+#pragma unroll
+    for (int nt = 0; nt < DEC_KEYS / 8; ++nt) {
+      float pv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int h = i >> 1;
+        pv[i] = mnew[h] == -INFINITY ? 0.f : exp2f(sc[nt][i] - mnew[h]);
+        lrow[h] += pv[i];
+      }
+      const int kk = nt >> 1, hi = nt & 1;
+      pa[kk][2 * hi] = pack_bf16(pv[0], pv[1]);
+      pa[kk][2 * hi + 1] = pack_bf16(pv[2], pv[3]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < DEC_KEYS / 16; ++kk) {
+      if (kk * 16 >= nk) break;
+      const uint32_t row_addr = lp::smem_u32(&Vw[kk * 16 + (lane & 15)][0]);
+#pragma unroll
+      for (int dt = 0; dt < DT; ++dt) {
+        uint32_t b0, b1;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                     : "=r"(b0), "=r"(b1)
+                     : "r"(row_addr + dt * 16));
+        mma_bf16_16816(o[dt], pa[kk], b0, b1);
+      }
+    }
+    __syncwarp();   // this warp's K/V slice is restaged for its next chunk
+  }
+  // merge the warps' partial softmax states (rows = heads of the group)
+  __syncthreads();
+  float* Om = reinterpret_cast<float*>(dec_smem);    // [ATT_WARPS][16][HD], reuses the K/V slices
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float lsum = lrow[h];
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+    if (cq == 0) {
+      sm_m[warp][r0 + 8 * h] = mrow[h];
+      sm_l[warp][r0 + 8 * h] = lsum;
+    }
+    float* orow = Om + ((size_t)warp * 16 + r0 + 8 * h) * HD + cq;
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+      orow[dt * 8] = o[dt][2 * h];
+      orow[dt * 8 + 1] = o[dt][2 * h + 1];
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
+    const int row = idx / HD, d = idx % HD;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < ATT_WARPS; ++w) mx = fmaxf(mx, sm_m[w][row]);
+    float den = 0.f, num = 0.f;
+#pragma unroll
+    for (int w = 0; w < ATT_WARPS; ++w) {
+      if (sm_m[w][row] == -INFINITY) continue;
+      const float f = exp2f(sm_m[w][row] - mx);
+      den += sm_l[w][row] * f;
+      num += Om[((size_t)w * 16 + row) * HD + d] * f;
+    }
+    out[((int64_t)t * H + kh * G + row) * HD + d] = __float2bfloat16_rn(num / den);
+  }
+}
+
 // greedy next token: argmax over logits[t, :] (lowest index wins ties)
 __global__ void argmax_kernel(const float* __restrict__ logits, int64_t V, int32_t* __restrict__ out,
                               float* __restrict__ top2 /* optional [T,2]: best, runner-up */) {
@@ -723,6 +893,27 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
     else
       LP_CUDA(lp::launch(attention_mma_kernel<128>, mgrid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv,
                          max_len, scale, oo));
+    return 0;
+  }
+  if (!many && (head_dim == 64 || head_dim == 128) && n_heads / n_kv <= 16) {
+    const dim3 dgrid((unsigned)T, (unsigned)n_kv);
+    if (head_dim == 64) {
+      constexpr size_t sm = (size_t)ATT_WARPS * 2 * DEC_KEYS * (64 + 8) * 2;
+      LP_CUDA(lp::launch(attention_mma_decode_kernel<64>, dgrid, blk, sm, s, qq, kk, vv, pos, seq, n_heads, n_kv,
+                         max_len, scale, oo));
+    } else {
+      constexpr size_t sm = (size_t)ATT_WARPS * 2 * DEC_KEYS * (128 + 8) * 2;
+      static uint64_t attr_dev = 0;
+      int dev = 0;
+      LP_CUDA(cudaGetDevice(&dev));
+      if (!(attr_dev >> dev & 1)) {
+        LP_CUDA(cudaFuncSetAttribute(attention_mma_decode_kernel<128>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr_dev |= 1ull << dev;
+      }
+      LP_CUDA(lp::launch(attention_mma_decode_kernel<128>, dgrid, blk, sm, s, qq, kk, vv, pos, seq, n_heads, n_kv,
+                         max_len, scale, oo));
+    }
     return 0;
   }
   const bool rpw = many;
