@@ -706,7 +706,8 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
   }
   // merge the warps' partial softmax states (rows = heads of the group)
   __syncthreads();
-  float* Om = reinterpret_cast<float*>(dec_smem);    // [ATT_WARPS][16][HD], reuses the K/V slices
+  constexpr int OP = HD + 4;                          // padded row: the fragment stores hit 32 banks
+  float* Om = reinterpret_cast<float*>(dec_smem);    // [ATT_WARPS][16][OP], reuses the K/V slices
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float lsum = lrow[h];
@@ -716,7 +717,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
       sm_m[warp][r0 + 8 * h] = mrow[h];
       sm_l[warp][r0 + 8 * h] = lsum;
     }
-    float* orow = Om + ((size_t)warp * 16 + r0 + 8 * h) * HD + cq;
+    float* orow = Om + ((size_t)warp * 16 + r0 + 8 * h) * OP + cq;
 #pragma unroll
     for (int dt = 0; dt < DT; ++dt) {
       orow[dt * 8] = o[dt][2 * h];
@@ -735,7 +736,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
       if (sm_m[w][row] == -INFINITY) continue;
       const float f = exp2f(sm_m[w][row] - mx);
       den += sm_l[w][row] * f;
-      num += Om[((size_t)w * 16 + row) * HD + d] * f;
+      num += Om[((size_t)w * 16 + row) * OP + d] * f;
     }
     out[((int64_t)t * H + kh * G + row) * HD + d] = __float2bfloat16_rn(num / den);
   }
