@@ -58,3 +58,29 @@ def test_request_rows_and_allocation_from_events():
     assert abs(rows[0][2] - 0.04) < 1e-12 and rows[0][3] == 0.07
     assert rows[1][2] is None and rows[1][3] is None
     assert W.allocation_samples(events) == [(0.0, 0), (0.0, 2)]
+
+
+def test_plan_files_match_reference_plan(tmp_path):
+    """tools/plan_measure.py writes the reference's `plan` files
+    (cli.py:288-339): schedule.txt / pipelines.txt must equal the
+    reference's lines for the same (n, k, b) (golden grid, dumped from the
+    reference), with the measured lines only appended to summary.txt."""
+    import json
+    import sys
+    sys.path.insert(0, str(Path(__file__).parent.parent / "tools"))
+    import plan_measure as PM
+
+    from paper_2502_09922_b200 import scaleout as SO
+    grid = {(g["n"], g["k"], g["b"]): g for g in
+            json.loads((Path(__file__).parent / "golden" / "schedules.json").read_text())["grid"]}
+    for n, k, b in ((8, 1, 16), (8, 2, 16), (4, 1, 4)):
+        plan = SO.plan_scale_out("llama3-8b" if b == 16 else "tiny", n, k, b)
+        fake = {"plan": plan, "transfer_s": 0.02, "completion_s": {r: 0.02 for r in plan.receivers},
+                "first_activation_s": 0.01, "nvlink_frac": 0.8}
+        out = tmp_path / f"{n}_{k}_{b}"
+        lines = PM.write_plan(out, "m", k, fake)
+        g = grid[(n, k, b)]
+        assert (out / "schedule.txt").read_text().splitlines() == g["schedule_lines"]
+        assert (out / "pipelines.txt").read_text().splitlines() == g["pipeline_lines"]
+        assert f"step_count: {g['summary']['step_count']}" in lines
+        assert any(ln.startswith("measured_transfer_s:") for ln in lines)
