@@ -7,6 +7,7 @@
 // accumulation everywhere (the oracle, oracle/llama.py, is the same network
 // in fp32 on the same bf16 weights).
 #include "lp_common.cuh"
+#include <cooperative_groups.h>
 #include "../../include/lambdapipe.h"
 
 namespace {
@@ -579,6 +580,11 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
 // four warps merge (m, l, O) through smem at the end.  The CUDA-core
 // lane-per-key loop took 28.7 us per 8B layer at B = 16, ctx 160
 // (tools/attn_perf.py): a chain of dependent loads per 32 keys.
+// Long contexts with few rows (flash-decoding): gridDim.z CTAs of one
+// thread-block cluster split a row's keys (CTA z takes the chunks of warps
+// z * ATT_WARPS ..), and each CTA merges a slice of the output from every
+// CTA's (m, l, O) through distributed shared memory -- no workspace, no
+// second kernel.
 constexpr int DEC_KEYS = 32;
 
 template <int HD>
@@ -595,6 +601,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
   lp::pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x, kh = blockIdx.y;
+  const int S = gridDim.z, split = blockIdx.z;       // key split over the cluster
   const int G = H / KV;
   const int L = pos[t] + 1;
   const int r0 = lane >> 2, cq = (lane & 3) * 2;
@@ -618,7 +625,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
   for (int i = 0; i < DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   const float sl2 = scale * 1.4426950408889634f;
-  for (int c0 = warp * DEC_KEYS; c0 < L; c0 += ATT_WARPS * DEC_KEYS) {
+  for (int c0 = (split * ATT_WARPS + warp) * DEC_KEYS; c0 < L; c0 += S * ATT_WARPS * DEC_KEYS) {
     const int nk = min(DEC_KEYS, L - c0);
     {   // lane j stages key c0 + j (zero past the context)
       const int4* kr = reinterpret_cast<const int4*>(kg + (int64_t)(c0 + lane) * HD);
@@ -725,6 +732,37 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
     }
   }
   __syncthreads();
+  if (S > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();                                   // every CTA's partial state is in its smem
+    for (int idx = split * blockDim.x + threadIdx.x; idx < G * HD; idx += S * blockDim.x) {
+      const int row = idx / HD, d = idx % HD;
+      float mx = -INFINITY;
+      for (int r = 0; r < S; ++r) {
+        const float (*rm)[16] = cluster.map_shared_rank(sm_m, r);
+#pragma unroll
+        for (int w = 0; w < ATT_WARPS; ++w) mx = fmaxf(mx, rm[w][row]);
+      }
+      float den = 0.f, num = 0.f;
+      for (int r = 0; r < S; ++r) {
+        const float (*rm)[16] = cluster.map_shared_rank(sm_m, r);
+        const float (*rl)[16] = cluster.map_shared_rank(sm_l, r);
+        const float* rO = cluster.map_shared_rank(Om, r);
+#pragma unroll
+        for (int w = 0; w < ATT_WARPS; ++w) {
+          const float mw = rm[w][row];
+          if (mw == -INFINITY) continue;
+          const float f = exp2f(mw - mx);
+          den += rl[w][row] * f;
+          num += rO[((size_t)w * 16 + row) * OP + d] * f;
+        }
+      }
+      out[((int64_t)t * H + kh * G + row) * HD + d] = __float2bfloat16_rn(num / den);
+    }
+    cluster.sync();                                   // peers stay resident until their smem is read
+    return;
+  }
   for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
     const int row = idx / HD, d = idx % HD;
     float mx = -INFINITY;
@@ -897,11 +935,20 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
     return 0;
   }
   if (!many && (head_dim == 64 || head_dim == 128) && n_heads / n_kv <= 16) {
-    const dim3 dgrid((unsigned)T, (unsigned)n_kv);
+    // key split over a cluster when the rows alone cannot fill the SMs and
+    // the cache can hold long contexts (short-context serving keeps S = 1)
+    unsigned S = 1;
+    if (max_len >= 1024)
+      while (S < 8 && (int64_t)T * n_kv * S * 2 <= 148 && (int64_t)S * 2 * ATT_WARPS * DEC_KEYS <= max_len) S *= 2;
+    const dim3 dgrid((unsigned)T, (unsigned)n_kv, S);
     if (head_dim == 64) {
       constexpr size_t sm = (size_t)ATT_WARPS * 2 * DEC_KEYS * (64 + 8) * 2;
-      LP_CUDA(lp::launch(attention_mma_decode_kernel<64>, dgrid, blk, sm, s, qq, kk, vv, pos, seq, n_heads, n_kv,
-                         max_len, scale, oo));
+      if (S > 1)
+        LP_CUDA(lp::launch_cluster_z(attention_mma_decode_kernel<64>, dgrid, blk, S, sm, s, qq, kk, vv, pos, seq,
+                                     n_heads, n_kv, max_len, scale, oo));
+      else
+        LP_CUDA(lp::launch(attention_mma_decode_kernel<64>, dgrid, blk, sm, s, qq, kk, vv, pos, seq, n_heads, n_kv,
+                           max_len, scale, oo));
     } else {
       constexpr size_t sm = (size_t)ATT_WARPS * 2 * DEC_KEYS * (128 + 8) * 2;
       static uint64_t attr_dev = 0;
@@ -912,8 +959,12 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr_dev |= 1ull << dev;
       }
-      LP_CUDA(lp::launch(attention_mma_decode_kernel<128>, dgrid, blk, sm, s, qq, kk, vv, pos, seq, n_heads, n_kv,
-                         max_len, scale, oo));
+      if (S > 1)
+        LP_CUDA(lp::launch_cluster_z(attention_mma_decode_kernel<128>, dgrid, blk, S, sm, s, qq, kk, vv, pos, seq,
+                                     n_heads, n_kv, max_len, scale, oo));
+      else
+        LP_CUDA(lp::launch(attention_mma_decode_kernel<128>, dgrid, blk, sm, s, qq, kk, vv, pos, seq, n_heads,
+                           n_kv, max_len, scale, oo));
     }
     return 0;
   }

@@ -68,9 +68,23 @@ def test_attention_matches_fp32(hd, H, KV, ctx, run):
     softmax.  T x KV >= 1024 selects the prefill variants: smem-staged row
     tiles when max_len's K/V fit (the last two cases; mixed-sequence tiles
     read global memory), else a warp per row."""
+    _check_attention(hd, H, KV, ctx, run, max(ctx) + 8)
+
+
+@pytest.mark.parametrize("hd,H,KV,ctx,max_len", [(128, 32, 8, [4000], 4096), (64, 4, 2, [1, 1500, 700], 1536),
+                                                  (128, 64, 8, [2048, 30], 2056), (128, 32, 8, [1, 5], 2048),
+                                                  (128, 8, 8, [1100, 257, 64, 1], 1200)])
+def test_attention_long_context_cluster_split(hd, H, KV, ctx, max_len):
+    """Few decode rows over a long-context cache: the keys of a row are split
+    over a thread-block cluster and merged through distributed shared memory
+    (CTAs that get no keys carry an empty softmax state)."""
+    _check_attention(hd, H, KV, ctx, 0, max_len)
+
+
+def _check_attention(hd, H, KV, ctx, run, max_len):
     import torch
     g = torch.Generator(device="cuda").manual_seed(hd + H + len(ctx))
-    seqs, max_len = len(ctx), max(ctx) + 8
+    seqs = len(ctx)
     kc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
     vc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
     pos = [c - 1 for c in ctx] + list(range(ctx[0] - 1, max(ctx[0] - run, -1), -1))

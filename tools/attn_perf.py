@@ -46,7 +46,7 @@ def run(H, KV, hd, seqs, ctx, prefill):
 
 
 for H, KV in ((32, 8), (64, 8)):
-    for seqs, ctx in ((16, 160), (16, 1024), (64, 160), (1, 4096)):
+    for seqs, ctx in ((16, 160), (16, 1024), (64, 160), (1, 4096), (4, 2048), (1, 32768)):
         run(H, KV, 128, seqs, ctx, False)
     for seqs, ctx in ((16, 128), (8, 512), (1, 2048)):
         run(H, KV, 128, seqs, ctx, True)
