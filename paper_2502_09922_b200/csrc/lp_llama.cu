@@ -937,9 +937,14 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
   if (!many && (head_dim == 64 || head_dim == 128) && n_heads / n_kv <= 16) {
     // key split over a cluster when the rows alone cannot fill the SMs and
     // the cache can hold long contexts (short-context serving keeps S = 1)
+    static const int64_t split_ctas = [] {
+      const char* e = getenv("LP_DEC_SPLIT_CTAS");   // tuning knob: grid size the split may grow to
+      return e ? (int64_t)atoll(e) : (int64_t)148;
+    }();
     unsigned S = 1;
     if (max_len >= 1024)
-      while (S < 8 && (int64_t)T * n_kv * S * 2 <= 148 && (int64_t)S * 2 * ATT_WARPS * DEC_KEYS <= max_len) S *= 2;
+      while (S < 8 && (int64_t)T * n_kv * S * 2 <= split_ctas && (int64_t)S * 2 * ATT_WARPS * DEC_KEYS <= max_len)
+        S *= 2;
     const dim3 dgrid((unsigned)T, (unsigned)n_kv, S);
     if (head_dim == 64) {
       constexpr size_t sm = (size_t)ATT_WARPS * 2 * DEC_KEYS * (64 + 8) * 2;

@@ -15,8 +15,8 @@ lib = N.lib()
 P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 
 
-def run(H, KV, hd, seqs, ctx, prefill):
-    max_len = ctx + 8
+def run(H, KV, hd, seqs, ctx, prefill, max_len=None):
+    max_len = max_len or ctx + 8
     kc = (torch.randn(seqs, KV, max_len, hd, device="cuda") * 0.5).to(torch.bfloat16)
     vc = torch.randn(seqs, KV, max_len, hd, device="cuda").to(torch.bfloat16)
     if prefill:   # every position of every sequence
@@ -41,9 +41,15 @@ def run(H, KV, hd, seqs, ctx, prefill):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / 200 * 1e3
     kv_bytes = (seqs * KV * ctx * hd * 2 * 2) if not prefill else seqs * KV * ctx * hd * 2 * 2
-    print(f"{'prefill' if prefill else 'decode '} H={H} KV={KV} seqs={seqs:3d} ctx={ctx:5d} rows={T:6d}: "
+    print(f"{'prefill' if prefill else 'decode '} H={H} KV={KV} seqs={seqs:3d} ctx={ctx:5d} max_len={max_len:5d} rows={T:6d}: "
           f"{us:8.1f} us  (K/V {kv_bytes / us / 1e3:7.1f} GB/s)", flush=True)
 
+
+if len(sys.argv) > 1 and sys.argv[1] == "split":   # decode rows vs the cluster key split (cache capacity 2048)
+    for H, KV in ((32, 8), (64, 8)):
+        for seqs, ctx in ((16, 160), (16, 1024), (16, 2000), (8, 160), (8, 2000), (4, 2000), (32, 1024), (1, 160)):
+            run(H, KV, 128, seqs, ctx, False, 2048)
+    sys.exit(0)
 
 for H, KV in ((32, 8), (64, 8)):
     for seqs, ctx in ((16, 160), (16, 1024), (64, 160), (1, 4096), (4, 2048), (1, 32768)):
