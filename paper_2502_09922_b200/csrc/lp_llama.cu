@@ -857,6 +857,40 @@ __global__ void handoff_kernel(const int4* __restrict__ src, int4* __restrict__ 
 
 }  // namespace
 
+template <int HD>
+constexpr size_t decode_smem() { return (size_t)ATT_WARPS * 2 * DEC_KEYS * (HD + 8) * 2; }
+
+// Per device, once: the smem opt-in, and the largest key-split cluster the
+// decode kernel may use -- 16 CTAs (non-portable) when the occupancy query
+// says such a cluster fits, else the portable 8.  -1 on a CUDA error.
+template <int HD>
+int decode_max_split(int dev) {
+  static int cached[64] = {};
+  if (dev < 64 && cached[dev]) return cached[dev];
+  auto kern = attention_mma_decode_kernel<HD>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)decode_smem<HD>()) != cudaSuccess)
+    return -1;
+  int best = 8;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, 1, 16);
+    cfg.blockDim = dim3(ATT_WARPS * 32);
+    cfg.dynamicSmemBytes = decode_smem<HD>();
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 16;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) best = 16;
+  }
+  cudaGetLastError();   // a refused query leaves no sticky error
+  if (dev < 64) cached[dev] = best;
+  return best;
+}
+
 extern "C" {
 
 int lp_handoff(const void* src, void* dst, int64_t bytes, uint32_t* flag, uint32_t value, uint32_t* scratch,
@@ -941,36 +975,24 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
       const char* e = getenv("LP_DEC_SPLIT_CTAS");   // tuning knob: grid size the split may grow to
       return e ? (int64_t)atoll(e) : (int64_t)148;
     }();
+    int dev = 0;
+    LP_CUDA(cudaGetDevice(&dev));
+    const int max_split = head_dim == 64 ? decode_max_split<64>(dev) : decode_max_split<128>(dev);
+    LP_CHECK(max_split > 0, "lp_attention: decode kernel attribute setup failed");
     unsigned S = 1;
     if (max_len >= 1024)
-      while (S < 8 && (int64_t)T * n_kv * S * 2 <= split_ctas && (int64_t)S * 2 * ATT_WARPS * DEC_KEYS <= max_len)
+      while ((int)S < max_split && (int64_t)T * n_kv * S * 2 <= split_ctas &&
+             (int64_t)S * 2 * ATT_WARPS * DEC_KEYS <= max_len)
         S *= 2;
     const dim3 dgrid((unsigned)T, (unsigned)n_kv, S);
-    if (head_dim == 64) {
-      constexpr size_t sm = (size_t)ATT_WARPS * 2 * DEC_KEYS * (64 + 8) * 2;
-      if (S > 1)
-        LP_CUDA(lp::launch_cluster_z(attention_mma_decode_kernel<64>, dgrid, blk, S, sm, s, qq, kk, vv, pos, seq,
-                                     n_heads, n_kv, max_len, scale, oo));
-      else
-        LP_CUDA(lp::launch(attention_mma_decode_kernel<64>, dgrid, blk, sm, s, qq, kk, vv, pos, seq, n_heads, n_kv,
-                           max_len, scale, oo));
-    } else {
-      constexpr size_t sm = (size_t)ATT_WARPS * 2 * DEC_KEYS * (128 + 8) * 2;
-      static uint64_t attr_dev = 0;
-      int dev = 0;
-      LP_CUDA(cudaGetDevice(&dev));
-      if (!(attr_dev >> dev & 1)) {
-        LP_CUDA(cudaFuncSetAttribute(attention_mma_decode_kernel<128>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        attr_dev |= 1ull << dev;
-      }
-      if (S > 1)
-        LP_CUDA(lp::launch_cluster_z(attention_mma_decode_kernel<128>, dgrid, blk, S, sm, s, qq, kk, vv, pos, seq,
-                                     n_heads, n_kv, max_len, scale, oo));
-      else
-        LP_CUDA(lp::launch(attention_mma_decode_kernel<128>, dgrid, blk, sm, s, qq, kk, vv, pos, seq, n_heads,
-                           n_kv, max_len, scale, oo));
-    }
+#define LP_DEC(HDV)                                                                                                 \
+  (S > 1 ? lp::launch_cluster_z(attention_mma_decode_kernel<HDV>, dgrid, blk, S, decode_smem<HDV>(), s, qq, kk, vv, \
+                                pos, seq, n_heads, n_kv, max_len, scale, oo)                                        \
+         : lp::launch(attention_mma_decode_kernel<HDV>, dgrid, blk, decode_smem<HDV>(), s, qq, kk, vv, pos, seq,    \
+                      n_heads, n_kv, max_len, scale, oo))
+    if (head_dim == 64) LP_CUDA(LP_DEC(64));
+    else LP_CUDA(LP_DEC(128));
+#undef LP_DEC
     return 0;
   }
   const bool rpw = many;

@@ -73,11 +73,13 @@ def test_attention_matches_fp32(hd, H, KV, ctx, run):
 
 @pytest.mark.parametrize("hd,H,KV,ctx,max_len", [(128, 32, 8, [4000], 4096), (64, 4, 2, [1, 1500, 700], 1536),
                                                   (128, 64, 8, [2048, 30], 2056), (128, 32, 8, [1, 5], 2048),
-                                                  (128, 8, 8, [1100, 257, 64, 1], 1200)])
+                                                  (128, 8, 8, [1100, 257, 64, 1], 1200),
+                                                  (64, 4, 2, [1, 3000, 4100], 4200), (128, 64, 8, [20000], 20480)])
 def test_attention_long_context_cluster_split(hd, H, KV, ctx, max_len):
     """Few decode rows over a long-context cache: the keys of a row are split
-    over a thread-block cluster and merged through distributed shared memory
-    (CTAs that get no keys carry an empty softmax state)."""
+    over a thread-block cluster (8, or 16 non-portable when it fits) and
+    merged through distributed shared memory (CTAs that get no keys carry an
+    empty softmax state)."""
     _check_attention(hd, H, KV, ctx, 0, max_len)
 
 
