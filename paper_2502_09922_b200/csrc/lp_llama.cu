@@ -977,8 +977,11 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
     }();
     int dev = 0;
     LP_CUDA(cudaGetDevice(&dev));
-    const int max_split = head_dim == 64 ? decode_max_split<64>(dev) : decode_max_split<128>(dev);
+    int max_split = head_dim == 64 ? decode_max_split<64>(dev) : decode_max_split<128>(dev);
     LP_CHECK(max_split > 0, "lp_attention: decode kernel attribute setup failed");
+    // 16-CTA clusters pay only for very long caches (1 x 32768 keys 136 -> 125 us;
+    // 1 x 4096 keys 20.5 -> 22.6 us, the 64-way merge outweighs the keys)
+    if (max_len < 16384 && max_split > 8) max_split = 8;
     unsigned S = 1;
     if (max_len >= 1024)
       while ((int)S < max_split && (int64_t)T * n_kv * S * 2 <= split_ctas &&
