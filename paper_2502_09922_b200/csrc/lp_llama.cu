@@ -587,7 +587,9 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
 // second kernel.
 constexpr int DEC_KEYS = 32;
 
-template <int HD>
+// NST = 2 (the split path): each warp double-buffers its chunks, cp.async
+// fetches chunk j + 1 into the other smem stage while the MMAs run on chunk j.
+template <int HD, int NST>
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
@@ -607,8 +609,30 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
   const int r0 = lane >> 2, cq = (lane & 3) * 2;
   const __nv_bfloat16* kg = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
   const __nv_bfloat16* vg = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
-  __nv_bfloat16 (*Kw)[KS] = reinterpret_cast<__nv_bfloat16 (*)[KS]>(dec_smem) + warp * 2 * DEC_KEYS;
-  __nv_bfloat16 (*Vw)[KS] = Kw + DEC_KEYS;
+  __nv_bfloat16 (*Kbase)[KS] = reinterpret_cast<__nv_bfloat16 (*)[KS]>(dec_smem) + warp * NST * 2 * DEC_KEYS;
+  const int cstep = S * ATT_WARPS * DEC_KEYS;
+  const int cstart = (split * ATT_WARPS + warp) * DEC_KEYS;
+  // lane j fetches key c + j of chunk c into stage st (zero-filled past the context)
+  auto fetch = [&](int c, int st) {
+    const bool in = c + lane < L;
+    const int64_t row = in ? c + lane : 0;
+    const uint32_t nb = in ? 16u : 0u;
+    const uint32_t kd = lp::smem_u32(&Kbase[st * 2 * DEC_KEYS + lane][0]);
+    const uint32_t vd = lp::smem_u32(&Kbase[st * 2 * DEC_KEYS + DEC_KEYS + lane][0]);
+    const __nv_bfloat16* ks = kg + row * HD;
+    const __nv_bfloat16* vs = vg + row * HD;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kd + 16 * i), "l"(ks + 8 * i), "r"(nb)
+                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vd + 16 * i), "l"(vs + 8 * i), "r"(nb)
+                   : "memory");
+    }
+  };
+  if constexpr (NST == 2) {
+    if (cstart < L) fetch(cstart, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   uint32_t qa[KSTEPS][4];
 #pragma unroll
   for (int ks = 0; ks < KSTEPS; ++ks) {
@@ -625,9 +649,16 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
   for (int i = 0; i < DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   const float sl2 = scale * 1.4426950408889634f;
-  for (int c0 = (split * ATT_WARPS + warp) * DEC_KEYS; c0 < L; c0 += S * ATT_WARPS * DEC_KEYS) {
+  int jc = 0;
+  for (int c0 = cstart; c0 < L; c0 += cstep, ++jc) {
     const int nk = min(DEC_KEYS, L - c0);
-    {   // lane j stages key c0 + j (zero past the context)
+    __nv_bfloat16 (*Kw)[KS] = Kbase + (NST == 2 ? (jc & 1) : 0) * 2 * DEC_KEYS;
+    __nv_bfloat16 (*Vw)[KS] = Kw + DEC_KEYS;
+    if constexpr (NST == 2) {
+      if (c0 + cstep < L) fetch(c0 + cstep, (jc + 1) & 1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");   // chunk jc has landed
+    } else {   // lane j stages key c0 + j (zero past the context)
       const int4* kr = reinterpret_cast<const int4*>(kg + (int64_t)(c0 + lane) * HD);
       const int4* vr = reinterpret_cast<const int4*>(vg + (int64_t)(c0 + lane) * HD);
       int4 kv[HD / 8], vv[HD / 8];
@@ -857,8 +888,8 @@ __global__ void handoff_kernel(const int4* __restrict__ src, int4* __restrict__ 
 
 }  // namespace
 
-template <int HD>
-constexpr size_t decode_smem() { return (size_t)ATT_WARPS * 2 * DEC_KEYS * (HD + 8) * 2; }
+template <int HD, int NST = 1>
+constexpr size_t decode_smem() { return (size_t)ATT_WARPS * NST * 2 * DEC_KEYS * (HD + 8) * 2; }
 
 // Per device, once: the smem opt-in, and the largest key-split cluster the
 // decode kernel may use -- 16 CTAs (non-portable) when the occupancy query
@@ -867,15 +898,19 @@ template <int HD>
 int decode_max_split(int dev) {
   static int cached[64] = {};
   if (dev < 64 && cached[dev]) return cached[dev];
-  auto kern = attention_mma_decode_kernel<HD>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)decode_smem<HD>()) != cudaSuccess)
+  if (cudaFuncSetAttribute(attention_mma_decode_kernel<HD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)decode_smem<HD>()) != cudaSuccess)
+    return -1;
+  auto kern = attention_mma_decode_kernel<HD, 2>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)decode_smem<HD, 2>()) !=
+      cudaSuccess)
     return -1;
   int best = 8;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(1, 1, 16);
     cfg.blockDim = dim3(ATT_WARPS * 32);
-    cfg.dynamicSmemBytes = decode_smem<HD>();
+    cfg.dynamicSmemBytes = decode_smem<HD, 2>();
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
@@ -989,9 +1024,9 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
         S *= 2;
     const dim3 dgrid((unsigned)T, (unsigned)n_kv, S);
 #define LP_DEC(HDV)                                                                                                 \
-  (S > 1 ? lp::launch_cluster_z(attention_mma_decode_kernel<HDV>, dgrid, blk, S, decode_smem<HDV>(), s, qq, kk, vv, \
-                                pos, seq, n_heads, n_kv, max_len, scale, oo)                                        \
-         : lp::launch(attention_mma_decode_kernel<HDV>, dgrid, blk, decode_smem<HDV>(), s, qq, kk, vv, pos, seq,    \
+  (S > 1 ? lp::launch_cluster_z(attention_mma_decode_kernel<HDV, 2>, dgrid, blk, S, decode_smem<HDV, 2>(), s, qq, \
+                                kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)                                 \
+         : lp::launch(attention_mma_decode_kernel<HDV, 1>, dgrid, blk, decode_smem<HDV>(), s, qq, kk, vv, pos, seq,  \
                       n_heads, n_kv, max_len, scale, oo))
     if (head_dim == 64) LP_CUDA(LP_DEC(64));
     else LP_CUDA(LP_DEC(128));
