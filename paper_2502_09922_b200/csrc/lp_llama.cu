@@ -1023,11 +1023,19 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
              (int64_t)S * 2 * ATT_WARPS * DEC_KEYS <= max_len)
         S *= 2;
     const dim3 dgrid((unsigned)T, (unsigned)n_kv, S);
+    // the double-buffered variant holds one CTA per SM: only while the grid is one wave
+    static const int dbuf_env = [] {
+      const char* e = getenv("LP_DEC_DBUF");
+      return e ? atoi(e) : 1;
+    }();
+    const bool dbuf = dbuf_env && (int64_t)T * n_kv <= 148;
 #define LP_DEC(HDV)                                                                                                 \
   (S > 1 ? lp::launch_cluster_z(attention_mma_decode_kernel<HDV, 2>, dgrid, blk, S, decode_smem<HDV, 2>(), s, qq, \
                                 kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)                                 \
-         : lp::launch(attention_mma_decode_kernel<HDV, 1>, dgrid, blk, decode_smem<HDV>(), s, qq, kk, vv, pos, seq,  \
-                      n_heads, n_kv, max_len, scale, oo))
+   : dbuf ? lp::launch(attention_mma_decode_kernel<HDV, 2>, dgrid, blk, decode_smem<HDV, 2>(), s, qq, kk, vv, pos,   \
+                       seq, n_heads, n_kv, max_len, scale, oo)                                                      \
+          : lp::launch(attention_mma_decode_kernel<HDV, 1>, dgrid, blk, decode_smem<HDV>(), s, qq, kk, vv, pos, seq, \
+                       n_heads, n_kv, max_len, scale, oo))
     if (head_dim == 64) LP_CUDA(LP_DEC(64));
     else LP_CUDA(LP_DEC(128));
 #undef LP_DEC
