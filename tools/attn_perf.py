@@ -45,6 +45,9 @@ def run(H, KV, hd, seqs, ctx, prefill, max_len=None):
           f"{us:8.1f} us  (K/V {kv_bytes / us / 1e3:7.1f} GB/s)", flush=True)
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "one":     # one decode config (ncu target): one SEQS CTX [MAX_LEN]
+    run(32, 8, 128, int(sys.argv[2]), int(sys.argv[3]), False, int(sys.argv[4]) if len(sys.argv) > 4 else None)
+    sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "split":   # decode rows vs the cluster key split (cache capacity 2048)
     for H, KV in ((32, 8), (64, 8)):
         for seqs, ctx in ((16, 160), (16, 1024), (16, 2000), (8, 160), (8, 2000), (4, 2000), (32, 1024), (1, 160)):
