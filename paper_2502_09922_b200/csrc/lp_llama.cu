@@ -612,21 +612,20 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
   __nv_bfloat16 (*Kbase)[KS] = reinterpret_cast<__nv_bfloat16 (*)[KS]>(dec_smem) + warp * NST * 2 * DEC_KEYS;
   const int cstep = S * ATT_WARPS * DEC_KEYS;
   const int cstart = (split * ATT_WARPS + warp) * DEC_KEYS;
-  // lane j fetches key c + j of chunk c into stage st (zero-filled past the context)
+  // chunk c -> stage st, coalesced: a warp instruction covers 512 contiguous
+  // bytes (HD = 128: two key rows), rows past the context are zero-filled
   auto fetch = [&](int c, int st) {
-    const bool in = c + lane < L;
-    const int64_t row = in ? c + lane : 0;
-    const uint32_t nb = in ? 16u : 0u;
-    const uint32_t kd = lp::smem_u32(&Kbase[st * 2 * DEC_KEYS + lane][0]);
-    const uint32_t vd = lp::smem_u32(&Kbase[st * 2 * DEC_KEYS + DEC_KEYS + lane][0]);
-    const __nv_bfloat16* ks = kg + row * HD;
-    const __nv_bfloat16* vs = vg + row * HD;
+    constexpr int R = HD / 8;                          // 16-byte units per key row
 #pragma unroll
-    for (int i = 0; i < HD / 8; ++i) {
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kd + 16 * i), "l"(ks + 8 * i), "r"(nb)
-                   : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vd + 16 * i), "l"(vs + 8 * i), "r"(nb)
-                   : "memory");
+    for (int i = 0; i < R; ++i) {
+      const int u = i * 32 + lane, row = u / R, col = u % R;
+      const bool in = c + row < L;
+      const int64_t src = (in ? (int64_t)(c + row) : 0) * HD + col * 8;
+      const uint32_t nb = in ? 16u : 0u;
+      const uint32_t kd = lp::smem_u32(&Kbase[st * 2 * DEC_KEYS + row][col * 8]);
+      const uint32_t vd = lp::smem_u32(&Kbase[st * 2 * DEC_KEYS + DEC_KEYS + row][col * 8]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(kd), "l"(kg + src), "r"(nb) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(vd), "l"(vg + src), "r"(nb) : "memory");
     }
   };
   if constexpr (NST == 2) {
