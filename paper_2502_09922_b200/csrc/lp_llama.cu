@@ -657,19 +657,21 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
       if (c0 + cstep < L) fetch(c0 + cstep, (jc + 1) & 1);
       asm volatile("cp.async.commit_group;" ::: "memory");
       asm volatile("cp.async.wait_group 1;" ::: "memory");   // chunk jc has landed
-    } else {   // lane j stages key c0 + j (zero past the context)
-      const int4* kr = reinterpret_cast<const int4*>(kg + (int64_t)(c0 + lane) * HD);
-      const int4* vr = reinterpret_cast<const int4*>(vg + (int64_t)(c0 + lane) * HD);
-      int4 kv[HD / 8], vv[HD / 8];
+    } else {   // coalesced register staging (zero past the context), same unit map as fetch()
+      constexpr int R = HD / 8;
+      int4 kv[R], vv[R];
 #pragma unroll
-      for (int i = 0; i < HD / 8; ++i) {
-        kv[i] = lane < nk ? kr[i] : make_int4(0, 0, 0, 0);
-        vv[i] = lane < nk ? vr[i] : make_int4(0, 0, 0, 0);
+      for (int i = 0; i < R; ++i) {
+        const int u = i * 32 + lane, row = u / R, col = u % R;
+        const int64_t src = (int64_t)(c0 + row) * HD + col * 8;
+        kv[i] = row < nk ? *reinterpret_cast<const int4*>(kg + src) : make_int4(0, 0, 0, 0);
+        vv[i] = row < nk ? *reinterpret_cast<const int4*>(vg + src) : make_int4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int i = 0; i < HD / 8; ++i) {
-        reinterpret_cast<int4*>(&Kw[lane][0])[i] = kv[i];
-        reinterpret_cast<int4*>(&Vw[lane][0])[i] = vv[i];
+      for (int i = 0; i < R; ++i) {
+        const int u = i * 32 + lane, row = u / R, col = u % R;
+        *reinterpret_cast<int4*>(&Kw[row][col * 8]) = kv[i];
+        *reinterpret_cast<int4*>(&Vw[row][col * 8]) = vv[i];
       }
     }
     __syncwarp();
@@ -1022,12 +1024,15 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
              (int64_t)S * 2 * ATT_WARPS * DEC_KEYS <= max_len)
         S *= 2;
     const dim3 dgrid((unsigned)T, (unsigned)n_kv, S);
-    // the double-buffered variant holds one CTA per SM: only while the grid is one wave
+    // the double-buffered variant holds one CTA per SM: only while the grid is
+    // one wave, and only for long caches -- in a short-context graph step its
+    // 139 KB of smem keeps the next kernel's PDL prologue off the SMs
+    // (8B B = 16 step 3.09 -> 3.12 ms with it, profiles/attn_decode_coalesced_ab_r01.txt)
     static const int dbuf_env = [] {
       const char* e = getenv("LP_DEC_DBUF");
       return e ? atoi(e) : 1;
     }();
-    const bool dbuf = dbuf_env && (int64_t)T * n_kv <= 148;
+    const bool dbuf = S > 1 || (dbuf_env && (int64_t)T * n_kv <= 148 && max_len >= 1024);
 #define LP_DEC(HDV)                                                                                                 \
   (S > 1 ? lp::launch_cluster_z(attention_mma_decode_kernel<HDV, 2>, dgrid, blk, S, decode_smem<HDV, 2>(), s, qq, \
                                 kk, vv, pos, seq, n_heads, n_kv, max_len, scale, oo)                                 \
