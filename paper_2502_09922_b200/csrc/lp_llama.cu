@@ -376,7 +376,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
-template <int HD>
+// NST = 2: K/V chunk j + 1 is fetched with cp.async into a second stage
+// (dynamic smem) while chunk j is on the tensor cores.
+template <int HD, int NST>
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
     const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
@@ -386,6 +388,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
   constexpr int DT = HD / 8;                 // PV n-tiles
   __shared__ __align__(16) __nv_bfloat16 Ks[MMA_KEYS][KS];
   __shared__ __align__(16) __nv_bfloat16 Vs[MMA_KEYS][KS];
+  extern __shared__ __align__(16) uint8_t att_dyn[];  // NST = 2: stage 1 (K then V)
   __shared__ int s_same, s_len, s_pos[MMA_ROWS];
   lp::pdl_wait();
   lp::pdl_trigger();
@@ -467,18 +470,48 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
   const int len = s_len;
   const __nv_bfloat16* kg = k_cache + ((int64_t)seq[t0] * KV + kh) * max_len * HD;
   const __nv_bfloat16* vg = v_cache + ((int64_t)seq[t0] * KV + kh) * max_len * HD;
-  for (int c0 = 0; c0 < len; c0 += MMA_KEYS) {
-    const int nk = min(MMA_KEYS, len - c0);
-    constexpr int V8 = HD / 8;
+  constexpr int V8 = HD / 8;
+  using Row = __nv_bfloat16[KS];
+  Row* const dynK = reinterpret_cast<Row*>(att_dyn);
+  Row* const dynV = dynK + MMA_KEYS;
+  auto fetch = [&](int c, int st) {   // zero-filled past len
+    Row* const dK = st ? dynK : Ks;
+    Row* const dV = st ? dynV : Vs;
     for (int i = threadIdx.x; i < MMA_KEYS * V8; i += blockDim.x) {
-      const int r = i / V8, c = i % V8;
-      int4 kv = make_int4(0, 0, 0, 0), vv = kv;
-      if (r < nk) {
-        kv = reinterpret_cast<const int4*>(kg + (int64_t)(c0 + r) * HD)[c];
-        vv = reinterpret_cast<const int4*>(vg + (int64_t)(c0 + r) * HD)[c];
+      const int r = i / V8, cc = i % V8;
+      const bool in = c + r < len;
+      const int64_t src = (in ? (int64_t)(c + r) : 0) * HD + cc * 8;
+      const uint32_t nb = in ? 16u : 0u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(lp::smem_u32(&dK[r][cc * 8])),
+                   "l"(kg + src), "r"(nb) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(lp::smem_u32(&dV[r][cc * 8])),
+                   "l"(vg + src), "r"(nb) : "memory");
+    }
+  };
+  if constexpr (NST == 2) {
+    fetch(0, 0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  int jc = 0;
+  for (int c0 = 0; c0 < len; c0 += MMA_KEYS, ++jc) {
+    const int nk = min(MMA_KEYS, len - c0);
+    Row* const Kc = (NST == 2 && (jc & 1)) ? dynK : Ks;
+    Row* const Vc = (NST == 2 && (jc & 1)) ? dynV : Vs;
+    if constexpr (NST == 2) {
+      if (c0 + MMA_KEYS < len) fetch(c0 + MMA_KEYS, (jc + 1) & 1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      for (int i = threadIdx.x; i < MMA_KEYS * V8; i += blockDim.x) {
+        const int r = i / V8, c = i % V8;
+        int4 kv = make_int4(0, 0, 0, 0), vv = kv;
+        if (r < nk) {
+          kv = reinterpret_cast<const int4*>(kg + (int64_t)(c0 + r) * HD)[c];
+          vv = reinterpret_cast<const int4*>(vg + (int64_t)(c0 + r) * HD)[c];
+        }
+        reinterpret_cast<int4*>(&Kc[r][0])[c] = kv;
+        reinterpret_cast<int4*>(&Vc[r][0])[c] = vv;
       }
-      reinterpret_cast<int4*>(&Ks[r][0])[c] = kv;
-      reinterpret_cast<int4*>(&Vs[r][0])[c] = vv;
     }
     __syncthreads();
     if (active) {
@@ -487,7 +520,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
 #pragma unroll
       for (int nt = 0; nt < MMA_KEYS / 8; ++nt) {
         sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-        const __nv_bfloat16* kr = &Ks[nt * 8 + r0][cq];
+        const __nv_bfloat16* kr = &Kc[nt * 8 + r0][cq];
 #pragma unroll
         for (int ks = 0; ks < KSTEPS; ++ks) {
           const uint32_t b0 = *reinterpret_cast<const uint32_t*>(kr + ks * 16);
@@ -542,7 +575,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
 #pragma unroll
       for (int kk = 0; kk < MMA_KEYS / 16; ++kk) {
         if (c0 + kk * 16 >= len) break;
-        const uint32_t row_addr = lp::smem_u32(&Vs[kk * 16 + (lane & 15)][0]);
+        const uint32_t row_addr = lp::smem_u32(&Vc[kk * 16 + (lane & 15)][0]);
 #pragma unroll
         for (int dt = 0; dt < DT; ++dt) {
           uint32_t b0, b1;
@@ -889,6 +922,9 @@ __global__ void handoff_kernel(const int4* __restrict__ src, int4* __restrict__ 
 
 }  // namespace
 
+template <int HD>
+constexpr size_t prefill_stage_bytes() { return (size_t)2 * MMA_KEYS * (HD + 8) * 2; }
+
 template <int HD, int NST = 1>
 constexpr size_t decode_smem() { return (size_t)ATT_WARPS * NST * 2 * DEC_KEYS * (HD + 8) * 2; }
 
@@ -996,11 +1032,34 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
     const dim3 mgrid((unsigned)((T + MMA_ROWS - 1) / MMA_ROWS), (unsigned)n_kv,
                      (unsigned)((G + ATT_WARPS - 1) / ATT_WARPS));
     const int Ti = (int)T;
+    static const int pdb = [] {
+      const char* e = getenv("LP_PREFILL_DBUF");
+      return e ? atoi(e) : 1;
+    }();
+    if (pdb) {
+      int dev = 0;
+      LP_CUDA(cudaGetDevice(&dev));
+      static uint64_t pattr = 0;
+      if (!(pattr >> dev & 1)) {
+        LP_CUDA(cudaFuncSetAttribute(attention_mma_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)prefill_stage_bytes<64>()));
+        LP_CUDA(cudaFuncSetAttribute(attention_mma_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)prefill_stage_bytes<128>()));
+        pattr |= 1ull << dev;
+      }
+      if (head_dim == 64)
+        LP_CUDA(lp::launch(attention_mma_kernel<64, 2>, mgrid, blk, prefill_stage_bytes<64>(), s, qq, kk, vv, pos,
+                           seq, Ti, n_heads, n_kv, max_len, scale, oo));
+      else
+        LP_CUDA(lp::launch(attention_mma_kernel<128, 2>, mgrid, blk, prefill_stage_bytes<128>(), s, qq, kk, vv, pos,
+                           seq, Ti, n_heads, n_kv, max_len, scale, oo));
+      return 0;
+    }
     if (head_dim == 64)
-      LP_CUDA(lp::launch(attention_mma_kernel<64>, mgrid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv,
+      LP_CUDA(lp::launch(attention_mma_kernel<64, 1>, mgrid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv,
                          max_len, scale, oo));
     else
-      LP_CUDA(lp::launch(attention_mma_kernel<128>, mgrid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv,
+      LP_CUDA(lp::launch(attention_mma_kernel<128, 1>, mgrid, blk, 0, s, qq, kk, vv, pos, seq, Ti, n_heads, n_kv,
                          max_len, scale, oo));
     return 0;
   }
