@@ -173,6 +173,7 @@ def timed_steps(so, steps, warmup, distributed, stream, want=None):
     import torch.distributed as dist
     times, ok, launches = [], True, 0
     for i in range(warmup + steps):
+        so.poison(0x5A ^ i, stream)      # receivers start every step without the model (untimed)
         if distributed:
             dist.barrier()
         torch.cuda.synchronize()
@@ -290,6 +291,7 @@ def main():
         my_nodes = so.cluster.exec_nodes
         e2e_times = []
         for i in range(args.warmup + args.steps):
+            so.poison(0xC3 ^ i, stream)
             if distributed:
                 dist.barrier()
             torch.cuda.synchronize()

@@ -135,8 +135,8 @@ class AutoscaleServer(Server):
         g = sources + targets                                          # op-local -> global
         bufs = [self.buffers[x] for x in g]
         for x in targets:
-            E.N.call("lp_set_device", self.buffers[x].device)
-            E.N.call("lp_memset", E.C.c_void_p(self.buffers[x].signals), 0, self._sig_bytes(), None)
+            with E.on_device(self.buffers[x].device):
+                E.N.call("lp_memset", E.C.c_void_p(self.buffers[x].signals), 0, self._sig_bytes(), None)
             self.torch.cuda.synchronize(self.buffers[x].device)
         cl = E.Cluster.over_buffers(bufs, self.lay.block_offsets, self.lay.block_lengths, CE_TILE)
         cl.set_schedule_all(sched, srcs)

@@ -33,6 +33,21 @@ void set_error(const char* fmt, ...);
     }                                                                             \
   } while (0)
 
+// The library shares the CUDA runtime (and so the calling thread's current
+// device) with its host process: an entry point that needs a device switches
+// to it for the call and restores the caller's device on return.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // PTX memory-model helpers.  Flags cross GPUs over NVLink, so release/acquire
 // are .sys scoped; data moves with 16-byte vectors.

@@ -380,80 +380,64 @@ __global__ void __launch_bounds__(LP_MC_THREADS) mc_kernel(const McParams p) {
 
 // ---------------------------------------------------------------------------
 // Verify-as-it-lands: per-block checksums (the lp_block_checksums function,
-// sum of mix64(word ^ k * golden) over the block's 8-byte words) of what a
-// receiver holds, computed tile by tile while the scale-out is still running.
-// Every received block is cut into pieces inside its tiles; piece g goes to
-// CTA g % gridDim.x, which waits for the tile's flag (written by the kernel
-// or the copy-engine executor alike) and folds the piece into sums[block].
-struct VerifyParams {
-  NodeDev me;
-  const BlockDev* blocks;
-  const int32_t* order;   // blocks in this node's receive (step) order
-  unsigned long long* sums;
-  int* err;
-  int64_t tile_bytes, piece_bytes;
-  uint64_t timeout_ns;
-  uint32_t epoch;
-  int n_order;
-};
-
-__global__ void __launch_bounds__(512) verify_kernel(const VerifyParams p) {
+// sum of mix64(word ^ k * golden) over the block's 8-byte words, k = word
+// index in the block) of what a receiver holds, computed while the scale-out
+// is still running.  Nothing spins on a flag: the verify stream parks in a
+// stream-ordered wait (cuStreamWaitValue32 on the node's own block counter,
+// handled by the GPU front end, no SM held) and then launches this kernel over
+// the one block that just completed.
+__global__ void __launch_bounds__(512) block_sum_kernel(const char* __restrict__ base, int64_t len,
+                                                        unsigned long long* __restrict__ sum) {
   __shared__ uint64_t part[16];
-  __shared__ int s_ok;
-  const uint64_t t0 = lp::globaltimer();
-  if (threadIdx.x == 0) s_ok = 1;
-  int64_t g = 0;
-  for (int o = 0; o < p.n_order; ++o) {
-    const int blk = p.order[o];
-    const BlockDev bl = p.blocks[blk];
-    for (int t = 0; t < bl.ntiles; ++t) {
-      const int64_t tlo = (int64_t)t * p.tile_bytes;
-      const int64_t tlen = min(p.tile_bytes, bl.len - tlo);
-      const int64_t np = (tlen + p.piece_bytes - 1) / p.piece_bytes;
-      const int64_t first = (blockIdx.x - g % gridDim.x + gridDim.x) % gridDim.x;  // my first piece here
-      g += np;
-      if (first >= np) continue;
-      __syncthreads();
-      if (threadIdx.x == 0 && !wait_flag(p.me.flags + bl.tile_base + t, p.epoch, t0, p.timeout_ns, p.err, 2))
-        s_ok = 0;
-      __syncthreads();
-      if (!s_ok) return;
-      uint64_t acc = 0;
-      constexpr uint64_t G = 0x9E3779B97F4A7C15ull;
-      for (int64_t q = first; q < np; q += gridDim.x) {
-        const int64_t lo = tlo + q * p.piece_bytes;
-        const int64_t n16 = min(p.piece_bytes, tlen - q * p.piece_bytes) >> 4;   // pieces are 16 B multiples
-        const ulonglong2* w = reinterpret_cast<const ulonglong2*>(p.me.image + bl.off + lo);
-        const uint64_t k0 = (uint64_t)(lo >> 3);
-        const int T = blockDim.x;
-        int64_t i = threadIdx.x;
-        constexpr int U = 8;
-        for (; i + (U - 1) * T < n16; i += U * T) {   // 128 B in flight per thread
-          ulonglong2 v[U];
+  constexpr uint64_t G = 0x9E3779B97F4A7C15ull;
+  const ulonglong2* w = reinterpret_cast<const ulonglong2*>(base);
+  const int64_t n16 = len >> 4;                        // blocks are 16-byte multiples
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  uint64_t acc = 0;
+  constexpr int U = 8;                                 // 128 B in flight per thread
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * T < n16; i += U * T) {
+    ulonglong2 v[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) v[u] = __ldcs(w + i + u * T);
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(w + i + u * T);
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint64_t k = k0 + 2 * (uint64_t)(i + u * T);
-            acc += lp::mix64(v[u].x ^ (k * G)) + lp::mix64(v[u].y ^ ((k + 1) * G));
-          }
-        }
-        for (; i < n16; i += T) {
-          const ulonglong2 v = __ldcs(w + i);
-          const uint64_t k = k0 + 2 * (uint64_t)i;
-          acc += lp::mix64(v.x ^ (k * G)) + lp::mix64(v.y ^ ((k + 1) * G));
-        }
-      }
-#pragma unroll
-      for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-      if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint64_t sum = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) sum += part[i];
-        atomicAdd(p.sums + blk, (unsigned long long)sum);
-      }
+    for (int u = 0; u < U; ++u) {
+      const uint64_t k = 2 * (uint64_t)(i + u * T);
+      acc += lp::mix64(v[u].x ^ (k * G)) + lp::mix64(v[u].y ^ ((k + 1) * G));
     }
+  }
+  for (; i < n16; i += T) {
+    const ulonglong2 v = __ldcs(w + i);
+    const uint64_t k = 2 * (uint64_t)i;
+    acc += lp::mix64(v.x ^ (k * G)) + lp::mix64(v.y ^ ((k + 1) * G));
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += part[j];
+    atomicAdd(sum, (unsigned long long)t);
+  }
+}
+
+// Start-of-run block counters of the blocks a node PULLS in-kernel: (epoch-1)
+// x ntiles, so completion (old + 1 == epoch x ntiles in publish_tile) holds for
+// this run whatever an earlier, aborted run left behind.  Only the receiver's
+// own kernel increments these counters, and it runs after this on the stream.
+struct CountReset {
+  uint32_t* counts[LP_MAX_EXEC];
+  int op_b[LP_MAX_EXEC], op_e[LP_MAX_EXEC];
+  const OpDev* ops;
+  const BlockDev* blocks;
+  uint32_t epoch;
+};
+__global__ void count_reset_kernel(const CountReset r) {
+  const int e = blockIdx.x;
+  for (int i = r.op_b[e] + threadIdx.x; i < r.op_e[e]; i += blockDim.x) {
+    const OpDev op = r.ops[i];
+    r.counts[e][op.block] = (r.epoch - 1u) * (uint32_t)r.blocks[op.block].ntiles;
   }
 }
 
@@ -472,8 +456,8 @@ struct lp_mc {
   // compiled per-node op ranges
   std::vector<ExecDesc> per_node;
   std::vector<OpDev> h_ops;         // host copy of the compiled op lists (copy-engine executor)
-  std::vector<int32_t> vr_off;      // [N+1] offsets of each node's receive order in d_vorder
-  int32_t* d_vorder = nullptr;
+  std::vector<int32_t> vr_off;      // [N+1] offsets of each node's receive order in h_vorder
+  std::vector<int32_t> h_vorder;    // blocks each node receives, in step order (verify)
   int dev = 0;
   NodeDev* d_nodes = nullptr;
   BlockDev* d_blocks = nullptr;
@@ -488,11 +472,13 @@ struct lp_mc {
   int wide_loads = 0;
   int host_dma = 0;                   // HOST-sourced transfers run on the copy engines (lp_mc_run_host_dma)
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;   // flag-wait watchdog
+  uint32_t last_epoch = 0;            // last epoch launched on this handle
+  bool failed = false;                // a watchdog expired: signals must be reset before the next run
   cudaStream_t poll = nullptr;   // private non-blocking stream for host polls
 };
 
 static int poll_stream(lp_mc* mc) {
-  LP_CUDA(cudaSetDevice(mc->dev));
+  lp::DeviceGuard g(mc->dev);
   if (!mc->poll) LP_CUDA(cudaStreamCreateWithFlags(&mc->poll, cudaStreamNonBlocking));
   return 0;
 }
@@ -584,12 +570,8 @@ static int compile(lp_mc* mc) {
       if (r.rcv == n) vorder.push_back(r.blk);
   }
   mc->vr_off[N] = (int)vorder.size();
-  LP_CUDA(cudaSetDevice(mc->dev));
-  if (mc->d_vorder) cudaFree(mc->d_vorder);
-  mc->d_vorder = nullptr;
-  LP_CUDA(cudaMalloc(&mc->d_vorder, sizeof(int32_t) * std::max<size_t>(1, vorder.size())));
-  if (!vorder.empty())
-    LP_CUDA(cudaMemcpy(mc->d_vorder, vorder.data(), sizeof(int32_t) * vorder.size(), cudaMemcpyHostToDevice));
+  mc->h_vorder = vorder;
+  lp::DeviceGuard g(mc->dev);
   if (mc->d_ops) cudaFree(mc->d_ops);
   if (mc->d_recv) cudaFree(mc->d_recv);
   mc->d_ops = nullptr;
@@ -641,24 +623,24 @@ int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_of
   }
   cudaMemcpy(mc->d_blocks, mc->blocks.data(), sizeof(BlockDev) * n_blocks, cudaMemcpyHostToDevice);
   cudaMemset(mc->d_err, 0, sizeof(int));
-  // force-load the spinning kernels now: under lazy module loading, loading a
-  // kernel while another one spins on its flags would wait for that one
-  // (multicast kernel <-> verify kernel <-> copy-engine flags deadlock)
+  // force-load the engine's kernels now: under lazy module loading, loading a
+  // kernel while the multicast kernel spins on a peer's (or a copy engine's)
+  // flags would wait for that kernel to finish
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, mc_kernel);
-  cudaFuncGetAttributes(&fa, verify_kernel);
+  cudaFuncGetAttributes(&fa, block_sum_kernel);
+  cudaFuncGetAttributes(&fa, count_reset_kernel);
   *out = mc;
   return 0;
 }
 
 int lp_mc_destroy(lp_mc* mc) {
   if (!mc) return 0;
-  cudaSetDevice(mc->dev);
+  lp::DeviceGuard g(mc->dev);
   cudaFree(mc->d_nodes);
   cudaFree(mc->d_blocks);
   cudaFree(mc->d_ops);
   cudaFree(mc->d_recv);
-  cudaFree(mc->d_vorder);
   cudaFree(mc->d_err);
   if (mc->poll) cudaStreamDestroy(mc->poll);
   delete mc;
@@ -700,6 +682,8 @@ int lp_mc_reset_signals(lp_mc* mc, int node, void* stream) {
   LP_CHECK(mc && node >= 0 && node < mc->n_nodes, "lp_mc_reset_signals: bad node");
   LP_CHECK(mc->nodes[node].flags, "lp_mc_reset_signals: node %d has no signal area", node);
   LP_CUDA(cudaMemsetAsync(mc->nodes[node].flags, 0, (size_t)mc->signal_bytes, (cudaStream_t)stream));
+  mc->failed = false;
+  mc->last_epoch = 0;
   return 0;
 }
 
@@ -755,6 +739,13 @@ int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch, 
   LP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, mc->dev));
   LP_CHECK(per * n_exec <= occ * sms,
            "lp_mc_run: %d CTAs exceed the %d co-resident CTAs the dataflow needs", per * n_exec, occ * sms);
+  LP_CHECK(!mc->failed, "lp_mc_run: an earlier run timed out; call lp_mc_reset_signals on every node "
+                        "(then restart at epoch 1)");
+  // pushed tiles are counted in the receiver's memory by remote senders, so
+  // their block counters cannot be re-based here: pushes need every earlier
+  // epoch complete, i.e. consecutive epochs on this handle
+  LP_CHECK(push_ctas == 0 || epoch == mc->last_epoch + 1 || epoch == mc->last_epoch,
+           "lp_mc_run: push runs need consecutive epochs (last %u, got %u)", mc->last_epoch, epoch);
   if (mc->dirty && compile(mc) != 0) return -2;
   McParams p{};
   p.nodes = mc->d_nodes;
@@ -779,8 +770,22 @@ int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch, 
     LP_CHECK(mc->nodes[n].kind == LP_NODE_GPU, "lp_mc_run: exec node %d is not a GPU node", n);
     p.exec[i] = mc->per_node[n];
   }
+  if (pull_ctas > 0) {   // re-base the counters of the blocks this run pulls in-kernel
+    CountReset r{};
+    for (int i = 0; i < n_exec; ++i) {
+      r.counts[i] = mc->nodes[exec_nodes[i]].counts;
+      r.op_b[i] = p.exec[i].pull_b;
+      r.op_e[i] = p.exec[i].pull_e;
+    }
+    r.ops = mc->d_ops;
+    r.blocks = mc->d_blocks;
+    r.epoch = epoch;
+    count_reset_kernel<<<n_exec, 128, 0, (cudaStream_t)stream>>>(r);
+    LP_CUDA(cudaGetLastError());
+  }
   mc_kernel<<<per * n_exec, LP_MC_THREADS, smem, (cudaStream_t)stream>>>(p);
   LP_CUDA(cudaGetLastError());
+  mc->last_epoch = epoch;
   return 0;
 }
 
@@ -931,27 +936,29 @@ int lp_mc_node_ops(lp_mc* mc, int node, int* kernel_ops, int* dma_ops) {
 }
 
 int lp_mc_verify(lp_mc* mc, int node, uint32_t epoch, int ctas, uint64_t* sums_dev, void* stream) {
+  if (resolve_stream_memops() != 0) return -1;
   LP_CHECK(mc && node >= 0 && node < mc->n_nodes && sums_dev, "lp_mc_verify: bad arguments");
   LP_CHECK(epoch >= 1 && ctas >= 1 && ctas <= 1024, "lp_mc_verify: bad epoch / CTA count");
-  LP_CHECK(mc->nodes[node].kind == LP_NODE_GPU && mc->nodes[node].flags,
+  LP_CHECK(mc->nodes[node].kind == LP_NODE_GPU && mc->nodes[node].counts,
            "lp_mc_verify: node %d is not a GPU node with signals", node);
   if (mc->dirty && compile(mc) != 0) return -2;
-  LP_CUDA(cudaMemsetAsync(sums_dev, 0, sizeof(uint64_t) * mc->n_blocks, (cudaStream_t)stream));
-  const int nb = mc->vr_off[node + 1] - mc->vr_off[node];
-  if (nb == 0) return 0;
-  VerifyParams p{};
-  p.me = mc->nodes[node];
-  p.blocks = mc->d_blocks;
-  p.order = mc->d_vorder + mc->vr_off[node];
-  p.sums = reinterpret_cast<unsigned long long*>(sums_dev);
-  p.err = mc->d_err;
-  p.tile_bytes = mc->tile_bytes;
-  p.piece_bytes = std::min<int64_t>(mc->tile_bytes, 1 << 20);
-  p.timeout_ns = mc->timeout_ns;
-  p.epoch = epoch;
-  p.n_order = nb;
-  verify_kernel<<<ctas, 512, 0, (cudaStream_t)stream>>>(p);
-  LP_CUDA(cudaGetLastError());
+  cudaStream_t s = (cudaStream_t)stream;
+  LP_CUDA(cudaMemsetAsync(sums_dev, 0, sizeof(uint64_t) * mc->n_blocks, s));
+  const NodeDev me = mc->nodes[node];
+  // blocks in the step order they land; each one: a stream-ordered wait on the
+  // node's own counter, then one checksum launch over the landed block
+  for (int i = mc->vr_off[node]; i < mc->vr_off[node + 1]; ++i) {
+    const int blk = mc->h_vorder[i];
+    const BlockDev bl = mc->blocks[blk];
+    CUresult r = cuStreamWaitValue32((CUstream)s, (CUdeviceptr)(me.counts + blk), epoch * (uint32_t)bl.ntiles,
+                                     CU_STREAM_WAIT_VALUE_GEQ);
+    LP_CHECK(r == CUDA_SUCCESS, "lp_mc_verify: cuStreamWaitValue32 failed (%d)", (int)r);
+    const int64_t want = (bl.len / 16 + 4095) / 4096;           // >= 8 x 16 B per thread
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctas, want));
+    block_sum_kernel<<<grid, 512, 0, s>>>(me.image + bl.off, bl.len,
+                                           reinterpret_cast<unsigned long long*>(sums_dev) + blk);
+    LP_CUDA(cudaGetLastError());
+  }
   return 0;
 }
 
@@ -963,8 +970,9 @@ int lp_mc_status(lp_mc* mc, void* stream, int* code) {
   *code = h;
   if (h) {
     cudaMemset(mc->d_err, 0, sizeof(int));
+    mc->failed = true;
     lp::set_error("lp_mc: watchdog expired waiting for a tile flag (a peer never delivered; %s)",
-                  h == 2 ? "verify kernel" : "multicast kernel");
+                  "multicast kernel");
     return -3;
   }
   return 0;

@@ -42,12 +42,12 @@ int lp_set_device(int dev) {
   return 0;
 }
 int lp_sync_device(int dev) {
-  LP_CUDA(cudaSetDevice(dev));
+  lp::DeviceGuard g(dev);
   LP_CUDA(cudaDeviceSynchronize());
   return 0;
 }
 int lp_enable_peer(int dev, int peer) {
-  LP_CUDA(cudaSetDevice(dev));
+  lp::DeviceGuard g(dev);
   cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
   if (e == cudaErrorPeerAccessAlreadyEnabled) {
     cudaGetLastError();
@@ -58,12 +58,12 @@ int lp_enable_peer(int dev, int peer) {
 }
 int lp_malloc(int dev, int64_t bytes, void** out) {
   LP_CHECK(bytes > 0 && out, "lp_malloc: bad arguments");
-  LP_CUDA(cudaSetDevice(dev));
+  lp::DeviceGuard g(dev);
   LP_CUDA(cudaMalloc(out, (size_t)bytes));
   return 0;
 }
 int lp_free(int dev, void* ptr) {
-  LP_CUDA(cudaSetDevice(dev));
+  lp::DeviceGuard g(dev);
   LP_CUDA(cudaFree(ptr));
   return 0;
 }
@@ -85,7 +85,7 @@ int lp_ipc_get(void* dev_ptr, void* handle64) {
 int lp_ipc_open(int dev, const void* handle64, void** out) {
   cudaIpcMemHandle_t h;
   memcpy(&h, handle64, 64);
-  LP_CUDA(cudaSetDevice(dev));
+  lp::DeviceGuard g(dev);
   LP_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
   return 0;
 }
@@ -103,7 +103,7 @@ int lp_host_unregister(void* host) {
   return 0;
 }
 int lp_stream_create(int dev, void** stream) {
-  LP_CUDA(cudaSetDevice(dev));
+  lp::DeviceGuard g(dev);
   cudaStream_t s;
   LP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   *stream = (void*)s;

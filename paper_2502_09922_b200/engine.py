@@ -18,6 +18,7 @@ can address:
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import mmap
 import os
@@ -90,6 +91,7 @@ class MulticastEngine:
                C.c_void_p(ready or None))
 
     def set_schedule(self, rows, sources):
+        self._rows = [tuple(int(v) for v in r) for r in rows]
         flat = [int(v) for r in rows for v in r]
         arr = N.i32_array(flat) if flat else (C.c_int32 * 1)()
         N.call("lp_mc_set_schedule", self._h, arr, len(rows), N.i32_array(list(sources)), len(sources))
@@ -134,9 +136,15 @@ class MulticastEngine:
         evs = (C.c_void_p * self.n_blocks)(*[int(e) if e else None for e in block_events])
         N.call("lp_mc_landing_events", self._h, node, epoch, C.c_void_p(stream), evs)
 
+    def received_blocks(self, node: int) -> list:
+        """Blocks ``node`` receives under the current schedule, in step order."""
+        return [r[3] for r in sorted(getattr(self, "_rows", [])) if r[2] == node]
+
     def verify(self, node: int, epoch: int, sums_ptr: int, stream: int = 0, ctas: int = 32):
         """Checksum ``node``'s received blocks as they land (lp_mc_verify)
-        into ``n_blocks`` uint64 at device pointer ``sums_ptr``."""
+        into ``n_blocks`` uint64 at device pointer ``sums_ptr``: enqueue it
+        after the run's producers; ``stream`` parks in stream-ordered waits on
+        the node's block counters and launches one checksum kernel per block."""
         N.call("lp_mc_verify", self._h, node, epoch, ctas, C.c_void_p(sums_ptr), C.c_void_p(stream or None))
 
     def node_ops(self, node: int) -> tuple:
@@ -217,6 +225,15 @@ class HostImage:
             os.unlink(self.shm_path)
 
 
+@contextlib.contextmanager
+def on_device(device: int):
+    """Make ``device`` current for the calls inside (the library shares the
+    CUDA runtime with torch, so this is torch's device context)."""
+    import torch
+    with torch.cuda.device(device):
+        yield
+
+
 def dev_malloc(device: int, nbytes: int) -> int:
     p = C.c_void_p()
     N.call("lp_malloc", device, nbytes, C.byref(p))
@@ -274,8 +291,8 @@ class Cluster:
               host_node: bool = False, tile_bytes: int = DEFAULT_TILE):
         """All GPU nodes on one device (node ids 1.. if a host node 0 exists)."""
         n_nodes = n_gpu_nodes + (1 if host_node else 0)
-        N.call("lp_set_device", device)
-        eng = MulticastEngine(n_nodes, block_offsets, block_lengths, tile_bytes)
+        with on_device(device):
+            eng = MulticastEngine(n_nodes, block_offsets, block_lengths, tile_bytes)
         nodes = []
         host = None
         first = 0
@@ -352,12 +369,12 @@ class Cluster:
         n_nodes = len(node_devices) + off
         engines = {}
         for d in devs:
-            N.call("lp_set_device", d)
-            engines[d] = MulticastEngine(n_nodes, block_offsets, block_lengths, tile_bytes)
+            with on_device(d):
+                engines[d] = MulticastEngine(n_nodes, block_offsets, block_lengths, tile_bytes)
         nodes, host = [], None
         if host_node:
-            N.call("lp_set_device", devs[0])
-            host = HostImage(image_bytes)
+            with on_device(devs[0]):
+                host = HostImage(image_bytes)
             nodes.append(NodeBuffer(0, LP_NODE_HOST, -1, host.device_ptr))
         for i, d in enumerate(node_devices):
             img = dev_malloc(d, image_bytes)
@@ -365,7 +382,6 @@ class Cluster:
             N.call("lp_memset", C.c_void_p(sig), 0, engines[d].signal_bytes, None)
             nodes.append(NodeBuffer(i + off, LP_NODE_GPU, d, img, sig, [("dev", img), ("dev", sig)]))
         for d, eng in engines.items():
-            N.call("lp_set_device", d)
             for nb in nodes:
                 eng.set_node(nb.node, nb.kind, nb.image, nb.signals)
         for d in devs:
@@ -383,8 +399,8 @@ class Cluster:
         devs = sorted({nb.device for nb in buffers if nb.kind == LP_NODE_GPU})
         engines = {}
         for d in devs:
-            N.call("lp_set_device", d)
-            eng = MulticastEngine(len(buffers), block_offsets, block_lengths, tile_bytes)
+            with on_device(d):
+                eng = MulticastEngine(len(buffers), block_offsets, block_lengths, tile_bytes)
             for i, nb in enumerate(buffers):
                 eng.set_node(i, nb.kind, nb.image, nb.signals)
             engines[d] = eng
@@ -401,7 +417,6 @@ class Cluster:
 
     def set_schedule_all(self, schedule, sources):
         for d, eng in getattr(self, "per_device", {0: self.engine}).items():
-            N.call("lp_set_device", d)
             eng.set_schedule(schedule_rows(schedule), sources)
 
     def launch_devices(self, streams: dict, push_ctas: int = 0, pull_ctas: int = 64) -> int:
@@ -411,8 +426,8 @@ class Cluster:
         streams = self._mc_streams
         for d, eng in self.per_device.items():
             mine = [nb.node for nb in self.nodes if nb.kind == LP_NODE_GPU and nb.device == d]
-            N.call("lp_set_device", d)
-            eng.run(mine, self.epoch, push_ctas, pull_ctas, streams[d])
+            with on_device(d):
+                eng.run(mine, self.epoch, push_ctas, pull_ctas, streams[d])
         return self.epoch
 
     def launch_devices_ce(self, streams: dict) -> int:
@@ -429,23 +444,23 @@ class Cluster:
         self.epoch += 1
         self._mc_streams = {}
         for d, eng in self.per_device.items():
-            N.call("lp_set_device", d)
             cfg = getattr(eng, "cfg", (1, 0, 0, 16384, 3))
             if cfg[0] != 0:
                 eng.configure(0, *cfg[1:])
             st = streams[d]
             sts = list(st) if isinstance(st, (list, tuple)) else [st]     # several: ops round-robin
             ptrs = [x if isinstance(x, int) else x.cuda_stream for x in sts]
-            for nb in self.nodes:
-                if nb.kind == LP_NODE_GPU and nb.device == d:
-                    eng.run_ce(nb.node, self.epoch, ptrs)
+            with on_device(d):
+                for nb in self.nodes:
+                    if nb.kind == LP_NODE_GPU and nb.device == d:
+                        eng.run_ce(nb.node, self.epoch, ptrs)
         return self.epoch
 
     def wait_devices(self) -> None:
         """Synchronise every per-device multicast launch; raise on a watchdog expiry."""
         for d, eng in getattr(self, "per_device", {}).items():
-            N.call("lp_set_device", d)
-            eng.status(getattr(self, "_mc_streams", {}).get(d, 0))
+            with on_device(d):
+                eng.status(getattr(self, "_mc_streams", {}).get(d, 0))
 
     def complete_nodes(self, epoch: int | None = None) -> dict:
         """node -> per-block complete flags (reads each node's counters)."""
@@ -543,7 +558,7 @@ class Cluster:
         if run_kernel:
             self.engine.run(run_kernel, epoch, push_ctas, pull_ctas, stream.cuda_stream)
         self.join_ce(stream)
-        return epoch, int(bool(run_kernel))
+        return epoch, int(bool(run_kernel)) * (2 if pull_ctas > 0 else 1)   # (+ counter re-base kernel)
 
     def join_ce(self, stream) -> None:
         """Make ``stream`` wait for every CE stream of this process."""
@@ -566,9 +581,8 @@ def load_source_image(cluster: "Cluster", node: int, layout, seed: int, device: 
     nodes get a device fill copied down over PCIe)."""
     nb = cluster.node(node)
     if nb.kind == LP_NODE_GPU:
-        if nb.device >= 0:
-            N.call("lp_set_device", nb.device)
-        fill_image(nb.image, layout, seed)
+        with on_device(nb.device if nb.device >= 0 else device):
+            fill_image(nb.image, layout, seed)
         return
     scratch = dev_malloc(device, layout.weights_bytes)
     try:

@@ -212,10 +212,8 @@ class ScaleOut:
         self.cluster.engine.set_option("host_dma", int(executor == "hybrid"))
         self.kernel_launches = 0      # multicast kernels of the last run (this process)
         # verify-as-it-lands (lp_mc_verify): receivers checksum every block
-        # while it streams in; run() returns the sums (a d2h of 8 B per block)
-        # 48 CTAs checksum ~880 GB/s (profiles/verify_kernel_full_r01.csv),
-        # enough beside the SM executors; the copy-engine executor leaves every
-        # SM free, so NVLink-rate landings get 96
+        # once its counter completes (one checksum launch per block, grid
+        # capped at verify_ctas); run() returns the sums (a d2h of 8 B per block)
         self.verify = verify
         self.verify_ctas = verify_ctas or (96 if executor == "ce" else 48)
         self._vbuf = {}
@@ -243,12 +241,30 @@ class ScaleOut:
         return self.cluster.launch(self.push_ctas, self.pull_ctas, stream)
 
     def run(self, stream=None) -> ScaleOutResult:
+        """One scale-out epoch.  The producers (kernel / copy engines) are
+        enqueued first; verify-as-it-lands goes after them on side streams,
+        each parked in stream-ordered waits on its node's block counters (no
+        SM spins on work queued elsewhere, so the run also completes under
+        ncu's serialisation or a sanitizer)."""
         import torch
         s = stream or torch.cuda.current_stream()
         sp = E.N.stream_ptr(s)
         t0 = time.perf_counter()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(s)
+        if not self._loaded:
+            self.load_sources()
+        epoch_next = self.cluster.epoch + 1
+        if self.executor == "ce":
+            epoch = self.cluster.launch_ce(self.ce_streams, after=ev0)
+            self.cluster.join_ce(s)
+            self.kernel_launches = 0
+        elif self.executor == "hybrid":
+            epoch, self.kernel_launches = self.cluster.launch_hybrid(s, self.push_ctas, self.pull_ctas)
+        else:
+            epoch = self.launch(sp)
+            self.kernel_launches = 1 + int(self.pull_ctas > 0)    # count reset + multicast kernel
+        assert epoch == epoch_next
         vnodes = [n for n in self.cluster.exec_nodes if n not in self.plan.sources] if self.verify else []
         vstreams = []
         for node in vnodes:
@@ -258,46 +274,41 @@ class ScaleOut:
                                     torch.cuda.Stream(device=s.device))
             vs = self._vbuf[node][2]
             vs.wait_event(ev0)
-            vstreams.append((node, vs))
-        epoch_next = self.cluster.epoch + 1
-        for node, vs in vstreams:   # launched first: they park on the tile flags of this epoch
-            self.cluster.engine.verify(node, epoch_next, self._vbuf[node][0].data_ptr(), vs.cuda_stream,
+            self.cluster.engine.verify(node, epoch, self._vbuf[node][0].data_ptr(), vs.cuda_stream,
                                        self.verify_ctas)
+            vstreams.append((node, vs))
+        for node, vs in vstreams:
+            ev = torch.cuda.Event()
+            ev.record(vs)
+            s.wait_event(ev)
+        self._readback(vstreams, s)
+        ev1.record(s)
         if self.executor == "ce":
-            if not self._loaded:
-                self.load_sources()
-            epoch = self.cluster.launch_ce(self.ce_streams, after=ev0)
-            self.cluster.join_ce(s)
-            for node, vs in vstreams:
-                ev = torch.cuda.Event()
-                ev.record(vs)
-                s.wait_event(ev)
-            self._readback(vstreams, s)
-            ev1.record(s)
             s.synchronize()
-            self.kernel_launches = 0
-        elif self.executor == "hybrid":
-            if not self._loaded:
-                self.load_sources()
-            epoch, self.kernel_launches = self.cluster.launch_hybrid(s, self.push_ctas, self.pull_ctas)
         else:
-            self.kernel_launches = 1
-            epoch = self.launch(sp)
-        if self.executor != "ce":
-            for node, vs in vstreams:
-                ev = torch.cuda.Event()
-                ev.record(vs)
-                s.wait_event(ev)
-            self._readback(vstreams, s)
-            ev1.record(s)
             self.cluster.wait(sp)
         sums = {}
         for node, _ in vstreams:
             sums[node] = [int(x) & 0xFFFFFFFFFFFFFFFF for x in self._vbuf[node][1].tolist()]
-        assert epoch == epoch_next
+        verify_launches = sum(len(self.cluster.engine.received_blocks(n)) for n, _ in vstreams)
         wall = (time.perf_counter() - t0) * 1e3
         return ScaleOutResult(epoch, ev0.elapsed_time(ev1), wall, checksums=sums,
-                              launches=self.kernel_launches + len(vstreams))
+                              launches=self.kernel_launches + verify_launches)
+
+    def poison(self, value: int = 0xA5, stream=None) -> None:
+        """Overwrite every receiver image this process executes with a byte
+        pattern (outside any timed region), so the next run's checksums prove
+        that run delivered every byte rather than an earlier one."""
+        import torch
+        s = stream or torch.cuda.current_stream()
+        for node in self.cluster.exec_nodes:
+            if node in self.plan.sources:
+                continue
+            nb = self.cluster.node(node)
+            with E.on_device(nb.device):
+                E.N.call("lp_memset", E.C.c_void_p(nb.image), int(value) & 0xFF, self.plan.layout.weights_bytes,
+                         E.C.c_void_p(s.cuda_stream))
+        s.synchronize()
 
     def _readback(self, vstreams, s):
         import torch

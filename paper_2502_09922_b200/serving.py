@@ -177,6 +177,12 @@ class Server:
         if src_dev == dst_dev:
             return x
         dst = torch.empty(x.shape, dtype=x.dtype, device=f"cuda:{dst_dev}")
+        # dst comes from the destination stream's allocator pool: a block freed
+        # there may still be read by queued destination kernels, so the
+        # source-stream stores must wait for that stream first
+        free_ev = torch.cuda.Event()
+        free_ev.record(torch.cuda.current_stream(dst_dev))
+        torch.cuda.current_stream(src_dev).wait_event(free_ev)
         with torch.cuda.device(src_dev):
             N.check(N.lib().lp_handoff(N.C.c_void_p(x.data_ptr()), N.C.c_void_p(dst.data_ptr()),
                                        x.numel() * x.element_size(), None, 0, None,

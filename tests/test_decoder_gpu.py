@@ -2,9 +2,11 @@
 
 * tcgen05 GEMM vs a torch fp32 matmul of the same bf16 operands
   (tolerance: |err| <= 1e-3 * sqrt(K) * rms(x) * rms(w) * 4, fp32 accumulation);
-* the whole tiny Llama (prefill + KV-cache decode) vs the CPU fp32 oracle:
-  logits within LOGIT_TOL, greedy tokens identical wherever the oracle's
-  top-1/top-2 margin exceeds 2 x LOGIT_TOL.
+* the whole tiny Llama (prefill + KV-cache decode) vs the CPU oracle:
+  logits within LOGIT_TOL of the bf16-faithful oracle (and LOGIT_TOL_FP32 of
+  the transformers-pinned fp32 one); greedy tokens identical at EVERY
+  generated position of the committed prompts (tests/golden/prompts_tiny.json,
+  whose oracle margins clear the gate everywhere).
 """
 import math
 
@@ -16,7 +18,8 @@ from paper_2502_09922_b200 import image as I
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_TOL = 0.08   # absolute, on logits of std ~1.5 (bf16 activations at GEMM inputs)
+LOGIT_TOL = 0.02        # absolute vs the bf16-faithful oracle (logit std ~1.15); fixture gate 0.05
+LOGIT_TOL_FP32 = 0.1    # absolute vs the fp32 oracle (the bf16 roundings themselves move logits ~0.06)
 
 
 def _ptr(t):
@@ -134,30 +137,42 @@ def test_tiny_prefill_and_decode_match_oracle(tiny):
     import torch
     from oracle import llama as OL
     from paper_2502_09922_b200.llama import LlamaExecutor
+    from parity import assert_tokens, entries
     cfg, lay, W, ptr = tiny
-    prompt = np.random.default_rng(1).integers(0, cfg.vocab, 24).astype(np.int64)
+    e = next(x for x in entries(12) if len(x["prompt"]) == 24)
+    prompt = np.asarray(e["prompt"], dtype=np.int64)
     ex = LlamaExecutor(lay, ptr, 0, max_seqs=2, max_len=64)
     toks = torch.as_tensor(prompt, dtype=torch.int32, device="cuda")
     pos = torch.arange(len(prompt), dtype=torch.int32, device="cuda")
     seq = torch.zeros(len(prompt), dtype=torch.int32, device="cuda")
     _, logits = ex.forward(tokens=toks, pos=pos, seq=seq)
-    _, ref = OL.forward(cfg, W, prompt)
+    _, ref = OL.forward(cfg, W, prompt, bf16=True)
+    _, ref32 = OL.forward(cfg, W, prompt)
     err = (logits.cpu() - ref).abs().max().item()
+    err32 = (logits.cpu() - ref32).abs().max().item()
+    print(f"tiny prefill logits: max |gpu - bf16 oracle| {err:.5f}, |gpu - fp32 oracle| {err32:.5f}")
     assert err < LOGIT_TOL, err
-    # greedy decode through the KV cache vs oracle full recompute
-    gen_ref, margins = OL.greedy(cfg, W, prompt, 8)
+    assert err32 < LOGIT_TOL_FP32, err32
+    # greedy decode through the KV cache: all 16 positions
     tok, _ = ex.greedy(logits[-1:])
     out = [int(tok.item())]
-    for step in range(7):
+    for step in range(len(e["greedy"]) - 1):
         p = torch.tensor([len(prompt) + step], dtype=torch.int32, device="cuda")
         _, lg = ex.forward(tokens=tok, pos=p, seq=seq[:1])
         tok, _ = ex.greedy(lg)
         out.append(int(tok.item()))
-    for i, (a, b) in enumerate(zip(out, gen_ref)):
-        if margins[i] > 2 * LOGIT_TOL:
-            assert a == b, (i, out, gen_ref, margins)
-        else:
-            break
+    assert assert_tokens(out, e, what="tiny KV-cache decode") == 16
+    # teacher-forced logits of the decode steps: one causal oracle pass
+    full = list(prompt) + out[:-1]
+    _, ref_all = OL.forward(cfg, W, full, bf16=True)
+    ex2 = LlamaExecutor(lay, ptr, 0, max_seqs=2, max_len=64)
+    n = len(full)
+    _, lg_all = ex2.forward(tokens=torch.as_tensor(full, dtype=torch.int32, device="cuda"),
+                            pos=torch.arange(n, dtype=torch.int32, device="cuda"),
+                            seq=torch.zeros(n, dtype=torch.int32, device="cuda"))
+    err_all = (lg_all.cpu() - ref_all).abs().max().item()
+    print(f"tiny prefill {n} tokens: max |gpu - bf16 oracle| {err_all:.5f}")
+    assert err_all < LOGIT_TOL
 
 
 def test_stage_split_equals_local(tiny):
@@ -181,18 +196,15 @@ def test_stage_split_equals_local(tiny):
 
 
 def test_generate_api_matches_oracle(tiny):
-    """serving.generate(): batched prefill + graph decode == oracle greedy."""
-    from oracle import llama as OL
+    """serving.generate(): batched prefill + graph decode == oracle greedy at
+    every one of 16 positions for three prompts of different lengths."""
     from paper_2502_09922_b200.llama import LlamaExecutor
     from paper_2502_09922_b200.serving import generate
+    from parity import assert_tokens, doc
     cfg, lay, W, ptr = tiny
-    rng = np.random.default_rng(11)
-    prompts = [rng.integers(0, cfg.vocab, 9 + 3 * i).tolist() for i in range(3)]
+    es = [e for e in doc()["prompts"] if len(e["prompt"]) in (9, 12, 15)]
+    assert len(es) == 3
     ex = LlamaExecutor(lay, ptr, 0, max_seqs=4, max_len=48)
-    outs = generate(ex, prompts, 8)
-    for p, got in zip(prompts, outs):
-        ref, margins = OL.greedy(cfg, W, p, 8)
-        for i, (a, b) in enumerate(zip(got, ref)):
-            if margins[i] < 2 * LOGIT_TOL:
-                break
-            assert a == b, (got, ref, margins)
+    outs = generate(ex, [e["prompt"] for e in es], 16)
+    compared = sum(assert_tokens(got, e, what=f"generate prompt {len(e['prompt'])}") for got, e in zip(outs, es))
+    assert compared == 48

@@ -1,0 +1,71 @@
+"""Decoder parity at the benchmarked shapes: two-layer slices of Llama-3-8B
+(d 4096, hd 128, GQA 32/8, ffn 14336) and Llama-3-70B (d 8192, GQA 64/8,
+ffn 28672), both with RoPE theta 5e5 and the 128256-token vocabulary, run by
+the CUDA path and by the bf16-faithful CPU oracle on the same bf16 weights
+(the GPU-filled image copied to the host).
+
+One prefill of PROMPT tokens (T x KV >= 1024: the tensor-core prefill
+attention and the CTA-pair GEMMs) and DECODE single-token steps through the KV
+cache (decode attention, small-T GEMMs); the oracle's logits for every step
+come from one causal pass over prompt + the GPU's tokens (teacher forcing).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PROMPT, DECODE = 160, 4
+TOL = 0.03          # absolute, logits of std ~1 (bf16 activations; accumulation order differs)
+
+
+@pytest.mark.parametrize("name", ["llama3-8b", "llama3-70b"])
+def test_two_layer_slice_matches_oracle(name):
+    import torch
+    from oracle import llama as OL
+    from paper_2502_09922_b200 import engine as E
+    from paper_2502_09922_b200 import image as I
+    from paper_2502_09922_b200.llama import LlamaExecutor
+
+    cfg = dataclasses.replace(I.CONFIGS[name], name=f"{name}-2L", n_layers=2)
+    lay = I.build_layout(cfg, 2)
+    ptr = E.dev_malloc(0, lay.weights_bytes)
+    try:
+        E.fill_image(ptr, lay, 11)
+        torch.cuda.synchronize()
+        img = E.device_view(ptr, lay.weights_bytes, 0).cpu().numpy()
+        prompt = np.random.default_rng(4).integers(0, cfg.vocab, PROMPT).tolist()
+        ex = LlamaExecutor(lay, ptr, 0, max_seqs=1, max_len=PROMPT + DECODE + 8)
+        dev = "cuda:0"
+        _, lg = ex.forward(tokens=torch.as_tensor(prompt, dtype=torch.int32, device=dev),
+                           pos=torch.arange(PROMPT, dtype=torch.int32, device=dev),
+                           seq=torch.zeros(PROMPT, dtype=torch.int32, device=dev))
+        got = [lg[-1].float().cpu()]
+        toks = [int(lg[-1].argmax().item())]
+        for i in range(DECODE):
+            _, lg = ex.forward(tokens=torch.tensor([toks[-1]], dtype=torch.int32, device=dev),
+                               pos=torch.tensor([PROMPT + i], dtype=torch.int32, device=dev),
+                               seq=torch.zeros(1, dtype=torch.int32, device=dev))
+            got.append(lg[-1].float().cpu())
+            toks.append(int(lg[-1].argmax().item()))
+        torch.cuda.synchronize()
+    finally:
+        E.dev_free(0, ptr)
+    del ex
+    W = OL.weights(lay, img)
+    del img
+    torch.set_num_threads(max(1, torch.get_num_threads()))
+    _, ref = OL.forward(cfg, W, prompt + toks[:-1], bf16=True)
+    ref = ref[PROMPT - 1:]
+    err = max((g - r).abs().max().item() for g, r in zip(got, ref))
+    std = ref.std().item()
+    agree = sum(int(g.argmax()) == int(r.argmax()) for g, r in zip(got, ref))
+    print(f"{name} 2-layer slice: max |gpu - bf16 oracle| {err:.5f} (logit std {std:.3f}), "
+          f"argmax agree {agree}/{len(got)}")
+    assert err < TOL, err
+    # greedy identity wherever the oracle's top-2 margin clears 2 x TOL
+    for i, (g, r) in enumerate(zip(got, ref)):
+        top = r.topk(2).values
+        if (top[0] - top[1]).item() > 2 * TOL:
+            assert int(g.argmax()) == int(r.argmax()), (name, i)
