@@ -14,18 +14,29 @@ Executor: scaleout.choose_executor — hybrid for host sources (PCIe hop as
 pinned DMA on the copy engines, NVLink relays in the multicast kernel).
 
 metric/value: aggregate delivered GB/s = N x model bytes / max-over-ranks
-device time of one scale-out (CUDA events around it on its stream).  At N >= 2
-the line also carries the GPU-sourced multicast (Llama-3-8B, GPU0 -> N-1
-peers, b = 32; BASELINE configs[1] at N = 8) as "gpu_source"; at N >= 3
-"execute_while_load" (Llama-3-8B, 2 GPU sources, λPipe pipelines serving a
-burst while the rest receive; tokens/s + TTFT), at N >= 4
-"execute_while_load_70b" (BASELINE configs[3] shape) and "bursty_trace"
-(configs[4]: the reference's synthetic spike trace with repeated scale-outs).
+device time of one scale-out (CUDA events around it on its stream), with the
+reference's λPipe binomial schedule at EVERY N.  Receivers are overwritten
+with a byte pattern before every step (untimed), so each step's checksums
+prove that step delivered the model.  At N >= 2 the line also carries
+"sharded_host" (our non-reference host-load plan, labelled as such) and the
+GPU-sourced multicast (Llama-3-8B, GPU0 -> N-1 peers, b = 32; BASELINE
+configs[1] at N = 8) as "gpu_source"; at N >= 3 "execute_while_load"
+(Llama-3-8B, 2 GPU sources, λPipe pipelines serving a burst while the rest
+receive; tokens/s + TTFT), at N >= 4 "execute_while_load_70b" (BASELINE
+configs[3] shape) and "bursty_trace" (configs[4]: the reference's synthetic
+spike trace with repeated scale-outs).
+
+cpu_baseline (rank 0, N = 1): the oracle's CPU restatement of the same
+scale-out over host buffers (full image), plus BASELINE.md §3's other CPU
+items: the unmodified reference planner's ms per plan and its simulator's
+wall time on the C5 trace (from baseline/_ref), and the CPU logits oracle's
+tokens/s.
 
 --impl reference: the reference has no data plane (pure-Python planner +
 cost-model simulator); its CPU path for this workload is the
 oracle's restatement of the schedule's byte movement (oracle/dataplane.c,
-all host cores), timed on a bounded sample.
+all host cores) over the same full config (config.same_config; a
+memory-bounded block prefix only if N + 1 images do not fit in host RAM).
 """
 
 from __future__ import annotations
@@ -110,30 +121,149 @@ def measured_peaks():
 # CPU path (oracle restatement) — reference arm and cpu_baseline
 
 
-def cpu_sample(n_nodes: int, threads: int, sample_blocks: int = 4):
-    """Time the oracle's CPU execution of the C3 schedule restricted to the
-    first ``sample_blocks`` blocks' transfers (bounded sample)."""
-    import numpy as np
-    from oracle import dataplane as D
-    from paper_2502_09922_b200 import scaleout as SO
-    plan = SO.plan_scale_out(C3_MODEL, n_nodes, 1, C3_BLOCKS, host_source=True)
-    lay = plan.layout
-    keep = set(range(sample_blocks))
-    lines = [ln for ln in plan.lines() if int(ln.split(",")[3]) in keep]
-    span = lay.block_offsets[sample_blocks - 1] + lay.block_lengths[sample_blocks - 1]
-    src = np.random.default_rng(0).integers(0, 255, span, dtype=np.uint8)
-    imgs = [src] + [np.zeros(span, np.uint8) for _ in range(n_nodes - 1)]
-    for im in imgs[1:]:
-        im[::4096] = 1   # fault the pages in before timing
-    offs, lens = lay.block_offsets[:sample_blocks], lay.block_lengths[:sample_blocks]
-    t0 = time.perf_counter()
-    D.execute(imgs, offs, lens, lines, [0], threads=threads)
-    dt = time.perf_counter() - t0
-    delivered = sum(lens) * (n_nodes - 1)
-    for im in imgs[1:]:
-        assert np.array_equal(im, src)
-    return delivered / dt / 1e9, dt, f"C3 schedule (n={n_nodes}, b={C3_BLOCKS}) restricted to blocks " \
-        f"0..{sample_blocks - 1} ({sum(lens) / 1e9:.2f} GB per receiver), {threads} threads"
+def mem_available() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+class CpuPort:
+    """The oracle's CPU restatement of the C3 scale-out (oracle/dataplane.c
+    lp_ref_execute: every transfer of the reference's λPipe schedule lines a
+    memcpy, transfers of a step on all host threads, one barrier per step)
+    over host buffers: node 0 = the host copy, nodes 1..N = receivers.  Runs
+    the FULL image whenever (N + 1) images fit in 80 % of MemAvailable, else
+    the longest block prefix that does (``same_config`` says which)."""
+
+    def __init__(self, n_gpus: int, threads: int):
+        import numpy as np
+        from paper_2502_09922_b200 import scaleout as SO
+        self.np = np
+        self.threads = threads
+        self.plan = SO.plan_scale_out(C3_MODEL, n_gpus + 1, 1, C3_BLOCKS, host_source=True)
+        lay = self.plan.layout
+        n = len(self.plan.nodes)
+        budget = 0.8 * mem_available()
+        nb = lay.plan.block_count
+        span = lambda k: lay.block_offsets[k - 1] + lay.block_lengths[k - 1]   # noqa: E731
+        while nb > 1 and n * span(nb) > budget:
+            nb -= 1
+        self.blocks = nb
+        self.same_config = nb == lay.plan.block_count
+        self.span = span(nb)
+        keep = set(range(nb))
+        self.lines = [ln for ln in self.plan.lines() if int(ln.split(",")[3]) in keep]
+        self.offs, self.lens = lay.block_offsets[:nb], lay.block_lengths[:nb]
+        self.delivered = sum(self.lens) * (n - 1)
+        seed = np.random.default_rng(0).integers(0, 255, 64 << 20, dtype=np.uint8)
+        self.src = np.empty(self.span, np.uint8)
+        for o in range(0, self.span, seed.size):
+            m = min(seed.size, self.span - o)
+            self.src[o:o + m] = seed[:m]
+        self.imgs = [self.src] + [np.empty(self.span, np.uint8) for _ in range(n - 1)]
+
+    def step(self) -> float:
+        from oracle import dataplane as D
+        t0 = time.perf_counter()
+        D.execute(self.imgs, self.offs, self.lens, self.lines, [0], threads=self.threads)
+        return time.perf_counter() - t0
+
+    def check(self) -> bool:
+        """Wipe a sample of blocks on every receiver, run one more scale-out,
+        and compare them with the source (a full compare of N x 26 GB would
+        take longer than the runs)."""
+        np = self.np
+        sample = sorted({0, self.blocks // 2, self.blocks - 1})
+        for im in self.imgs[1:]:
+            for b in sample:
+                im[self.offs[b]:self.offs[b] + self.lens[b]] = 0
+        self.step()
+        return all(np.array_equal(im[self.offs[b]:self.offs[b] + self.lens[b]],
+                                  self.src[self.offs[b]:self.offs[b] + self.lens[b]])
+                   for im in self.imgs[1:] for b in sample)
+
+    def sample(self) -> str:
+        what = "full image" if self.same_config else f"blocks 0..{self.blocks - 1} (memory-bounded prefix)"
+        return (f"C3 λPipe schedule (n={len(self.plan.nodes)}, b={C3_BLOCKS}) executed host->host, {what}: "
+                f"{sum(self.lens) / 1e9:.2f} GB per receiver, {self.threads} threads")
+
+
+def reference_cpu_items(n_gpus: int, threads: int) -> dict:
+    """BASELINE.md §3 CPU items beside the byte-movement port:
+    (1) the real reference planner's wall time per plan, (2) the real
+    reference simulator's run over the C5 burst trace — both from the
+    unmodified reference installed in baseline/_ref (absent: reported as
+    such) — and (4) the CPU logits oracle's tokens/s on the tiny model."""
+    out = {}
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "blockcast")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        try:
+            from blockcast import multicast as RM
+            from blockcast import pipeline as RP
+
+            def plan(model, size, layers, n, k, b):
+                p = RM.partition_blocks(RM.ModelSpec(model, size, layers), b)
+                nodes = list(range(n))
+                g = RM.attach_orders(RM.partition_subgroups(nodes, nodes[:k]), RM.k_way_orders(b, k))
+                sch = RM.compose_schedule(g, p)
+                o = RP.completion_ordered_groups(g, sch)
+                return [RP.assign_blocks_to_stages(x, [q.transfer_order for q in o], b, sch, i)
+                        for i, x in enumerate(RP.generate_pipelines(o))]
+            rows = {}
+            for label, args in (("c3_host_to_%d_b40" % n_gpus, ("llama2-13b", 26031728640, 40, n_gpus + 1, 1, 40)),
+                                ("c2_gpu0_to_7_b16", ("llama3-8b", 16060522496, 32, 8, 1, 16)),
+                                ("c4_70b_1_to_8_b80_k2", ("llama3-70b", 141107412992, 80, 8, 2, 80))):
+                reps, t0 = 0, time.perf_counter()
+                while reps < 3 or time.perf_counter() - t0 < 1.0:
+                    plan(*args)
+                    reps += 1
+                rows[label] = round((time.perf_counter() - t0) / reps * 1e3, 3)
+            out["reference_planner_ms_per_plan"] = rows
+            from blockcast import simengine as RS
+            from blockcast import workload as RW
+            trace = RW.synth_burst(0.05, 6.0, [120.0, 800.0, 1500.0], 1800.0, seed=4, spike_duration_s=60.0,
+                                   output_tokens=(16, 32))
+            t0 = time.perf_counter()
+            res = RS.run(RS.ClusterSpec(), [RM.ModelSpec("m0", 13476831232, 32)], "lambda_scale", trace,
+                         RS.AutoscalePolicy(), block_count=16)
+            out["reference_simulator"] = {"s": round(time.perf_counter() - t0, 3), "requests": len(trace),
+                                          "completed": res.report.requests_completed,
+                                          "workload": "C5 synth_burst (1800 s, seed 4), Llama-2-7B size, lambda_scale, b=16"}
+            out["reference_install"] = "baseline/_ref (pip --target from the unmodified reference)"
+        except Exception as e:  # noqa: BLE001
+            out["reference_error"] = f"{type(e).__name__}: {e}"
+    else:
+        out["reference_install"] = "absent (baseline/_ref not installed): planner/simulator items skipped"
+    try:
+        import torch
+        from oracle import dataplane as D
+        from oracle import llama as OL
+        from paper_2502_09922_b200 import image as I
+        torch.set_num_threads(threads)
+        cfg = I.CONFIGS["tiny"]
+        lay = I.build_layout(cfg, 4)
+        W = OL.weights(lay, D.fill_image(lay, 7))
+        prompt = list(range(1, 129))
+        t0 = time.perf_counter()
+        for _ in range(3):
+            OL.forward(cfg, W, prompt, bf16=True)
+        pre = 3 * 128 / (time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        OL.greedy(cfg, W, prompt[:32], 8, bf16=True)
+        dec = 8 / (time.perf_counter() - t0)
+        out["oracle_tokens_per_s"] = {"prefill": round(pre, 1), "decode_recompute": round(dec, 2),
+                                      "model": "tiny (4 layers, d=256)", "threads": threads,
+                                      "note": "oracle/llama.py bf16 mode; decode re-runs the causal forward "
+                                              "per token (no KV cache)"}
+    except Exception as e:  # noqa: BLE001
+        out["oracle_error"] = f"{type(e).__name__}: {e}"
+    return out
 
 
 def run_reference(args):
@@ -141,20 +271,25 @@ def run_reference(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    vals = []
-    sample = ""
+    port = CpuPort(args.gpus, threads)
+    times = []
     for i in range(args.warmup + args.steps):
-        gbps, dt, sample = cpu_sample(args.gpus + 1, threads, sample_blocks=2 if args.gpus > 4 else 3)
+        dt = port.step()
         if i >= args.warmup:
-            vals.append(gbps)
-    v = statistics.median(vals)
+            times.append(dt)
+    T = statistics.median(times)
+    ok = port.check()
+    v = port.delivered / T / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{C3_MODEL} bf16 host->{args.gpus} GPU scale-out (b={C3_BLOCKS}, k=1)",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(T * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"{C3_MODEL} bf16 scale-out from the host copy to {args.gpus} receiver(s), "
+                                   f"b={C3_BLOCKS}, k=1, λPipe schedule",
+                       "same_config": port.same_config,
                        "executor": "oracle/dataplane.c lp_ref_execute (CPU memcpy per transfer, barrier per step)"},
+            "byte_exact": ok,
             "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                             "sample": sample},
+                             "sample": port.sample()},
             "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -215,8 +350,9 @@ def main():
                     help="skip verify-as-it-lands (for ncu launch lists: ncu serialises kernels, so a kernel "
                          "waiting on copy-engine flags can never finish under it); bytes are then checked once "
                          "after the timed region")
-    ap.add_argument("--strategy", default="auto", choices=["auto", "lambda", "sharded_host"],
-                    help="host-sourced scale-out plan (auto = scaleout.choose_strategy)")
+    ap.add_argument("--strategy", default="lambda", choices=["lambda", "sharded_host"],
+                    help="host-sourced scale-out plan of the headline value (default: the reference's λPipe "
+                         "binomial schedule; sharded_host is always measured beside it at N >= 2)")
     ap.add_argument("--executor", default="auto", choices=["auto", "hybrid", "kernel", "ce"],
                     help="host-sourced scale-out executor (auto = scaleout.choose_executor)")
     ap.add_argument("--no-gpu-source", action="store_true")
@@ -248,9 +384,9 @@ def main():
     peaks = measured_peaks()
 
     # --- main workload: C3 host -> N GPUs -----------------------------------
-    strategy = SO.choose_strategy(True, N) if args.strategy == "auto" else args.strategy
+    strategy = args.strategy
     plans = {st: SO.plan_scale_out(C3_MODEL, N + 1, 1, C3_BLOCKS, host_source=True, strategy=st)
-             for st in {strategy, "lambda"}}
+             for st in ({strategy, "lambda", "sharded_host"} if N >= 2 else {strategy})}
     plan = plans[strategy]
     M = plan.layout.weights_bytes
     tiles = {"hybrid": SO.HYBRID_TILE, "kernel": 2 << 20, "ce": SO.CE_TILE}
@@ -393,10 +529,16 @@ def main():
         cpu = None
         if N == 1:
             try:
-                gb, dt, sample = cpu_sample(2, threads)
-                cpu = {"value": round(gb, 3), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample}
+                port = CpuPort(1, threads)
+                port.step()                                   # page faults
+                dt = statistics.median([port.step() for _ in range(2)])
+                cpu = {"value": round(port.delivered / dt / 1e9, 3), "unit": "GB/s", "cores": threads,
+                       "kind": "port", "sample": port.sample() + ", median of 2 steps after 1 warm-up",
+                       "same_config": port.same_config}
+                del port
             except Exception as e:  # noqa: BLE001
                 cpu = {"value": None, "unit": "GB/s", "cores": threads, "kind": "port", "sample": f"failed: {e}"}
+            cpu.update(reference_cpu_items(N, threads))
         host_rows = [ln.split(",") for ln in plan.lines() if ln.split(",")[1] == "0"]
         n_links = len({r[2] for r in host_rows})  # GPUs the host feeds = PCIe links in use
         achieved = h2d / (T * 1e-3) / 1e9       # host->GPU bytes per step / step time
@@ -451,6 +593,10 @@ def main():
             "cpu_baseline": cpu,
             "peaks": {"hbm_gbs": peaks.get("hbm_gbs"), "bf16_tflops": peaks.get("bf16_tflops")},
         }
+        if N >= 2 and "sharded_host/hybrid" in host_exec:
+            line["sharded_host"] = dict(host_exec["sharded_host/hybrid"], note=(
+                "NOT the reference schedule: every GPU DMAs a disjoint block shard over its own PCIe link and the "
+                "shards rotate over NVLink (scaleout.sharded_host_schedule); reported beside the λPipe headline"))
         if gpu_source:
             line["gpu_source"] = gpu_source
         if serving:

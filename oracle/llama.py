@@ -12,12 +12,12 @@ attention with scale 1/sqrt(hd), SwiGLU MLP, untied LM head.
 
 ``bf16=True`` is the bf16-faithful mode: the same network, but every tensor
 the CUDA path stores in bf16 is rounded to bf16 at the same point — the
-RMSNorm outputs (GEMM inputs), q/k after RoPE and v (the bf16 KV cache), the
-attention output and the SwiGLU product — while the residual stream, GEMM
-accumulation, softmax and logits stay fp32 (paper_2502_09922_b200/llama.py
-module doc).  RoPE angles follow the kernel's fp32 recipe
+RMSNorm outputs (GEMM inputs), q/k after RoPE (the bf16 K cache), the
+attention output and the SwiGLU product — v is rounded to fp16 (the fp16 V
+cache), while the residual stream, GEMM accumulation, softmax and logits stay
+fp32 (paper_2502_09922_b200/llama.py module doc).  RoPE angles follow the kernel's fp32 recipe
 (inv = 2^(-2j/hd * log2 theta), angle = float(pos) * inv).  What remains
-between the two is accumulation order and the kernels' bf16 rounding of the
+between the two is accumulation order and the kernels' fp16 rounding of the
 softmax probabilities inside attention, so greedy tokens agree wherever the
 oracle's top-1/top-2 margin clears a small gate (tests/golden/prompts_tiny.json
 holds prompts whose margins clear it at every generated position).
@@ -43,6 +43,12 @@ def _bf(t, on: bool):
     """Round to bf16 and back when the CUDA path stores ``t`` in bf16."""
     import torch
     return t.to(torch.bfloat16).to(torch.float32) if on else t
+
+
+def _h(t, on: bool):
+    """Round to fp16 and back (the V cache) when faithful."""
+    import torch
+    return t.to(torch.float16).to(torch.float32) if on else t
 
 
 def _rms(x, w, eps):
@@ -85,7 +91,7 @@ def forward(cfg, W: dict, tokens, layers=None, x=None, head: bool = True, bf16: 
         h = _bf(_rms(x, W[p + "attn_norm"], cfg.norm_eps), bf16)
         q = (h @ W[p + "wq"].T).view(T, H, hd)
         k = (h @ W[p + "wk"].T).view(T, KV, hd)
-        v = _bf((h @ W[p + "wv"].T).view(T, KV, hd), bf16)
+        v = _h((h @ W[p + "wv"].T).view(T, KV, hd), bf16)
         q = _bf(_rope(q, pos, cfg.rope_theta, bf16), bf16)
         k = _bf(_rope(k, pos, cfg.rope_theta, bf16), bf16)
         k = k.repeat_interleave(G, dim=1)

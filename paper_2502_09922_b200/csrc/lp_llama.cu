@@ -4,8 +4,8 @@
 // 0..pos of its own sequence), and greedy argmax.
 //
 // Numerics: weights bf16, residual stream fp32, GEMM inputs bf16, fp32
-// accumulation everywhere (the oracle, oracle/llama.py, is the same network
-// in fp32 on the same bf16 weights).
+// accumulation everywhere; the V cache and the softmax probabilities of P V
+// are fp16 (oracle/llama.py bf16=True rounds at the same points).
 #include "lp_common.cuh"
 #include <cooperative_groups.h>
 #include "../../include/lambdapipe.h"
@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(RMS_THREADS) rmsnorm_kernel(const float* __res
 
 // qkv: [T, (H + 2*KV) * hd] fp32.  HF Llama rotate_half RoPE: element j < hd/2
 // pairs with j + hd/2 at angle pos * theta^(-2j/hd).
-// q_out [T, H*hd] bf16; k/v appended to cache[seq][kv][pos][hd] bf16.
+// q_out [T, H*hd] bf16; k appended to k_cache[seq][kv][pos][hd] bf16, v to
+// v_cache (same layout) fp16 -- the P V product runs in fp16.
 //
 // One CTA per (token, group of 8 heads): the angle table (cos, sin of
 // pos * theta^(-2j/hd), j < hd/2) depends only on the token's position, so it
@@ -117,7 +118,7 @@ constexpr int ROPE_HEADS = 8;      // rotated heads per CTA
 __global__ void __launch_bounds__(ROPE_THREADS) rope_kv_kernel(
     const float* __restrict__ qkv, int H, int KV, int hd, const int32_t* __restrict__ pos,
     const int32_t* __restrict__ seq, float theta, __nv_bfloat16* __restrict__ q_out,
-    __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache, int64_t max_len) {
+    __nv_bfloat16* __restrict__ k_cache, __half* __restrict__ v_cache, int64_t max_len) {
   lp::pdl_wait();
   lp::pdl_trigger();
   const int t = blockIdx.x;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(ROPE_THREADS) rope_kv_kernel(
     const float* vsrc = row + (int64_t)(H + KV) * hd;
     for (int i = threadIdx.x; i < KV * hd; i += blockDim.x) {
       const int kh = i / hd, j = i % hd;
-      v_cache[(((int64_t)sq * KV + kh) * max_len + p) * hd + j] = __float2bfloat16_rn(vsrc[i]);
+      v_cache[(((int64_t)sq * KV + kh) * max_len + p) * hd + j] = __float2half_rn(vsrc[i]);
     }
   }
 }
@@ -174,18 +175,18 @@ constexpr int MAX_G = 8;
 constexpr int PV_BATCH = 8;
 
 template <int PER>
-__device__ __forceinline__ void load_v(const __nv_bfloat16* p, float (&f)[4]) {
+__device__ __forceinline__ void load_v(const __half* p, float (&f)[4]) {
   if constexpr (PER == 4) {
     const uint2 raw = *reinterpret_cast<const uint2*>(p);
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
     f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
   } else if constexpr (PER == 2) {
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(p));
     f[0] = a.x; f[1] = a.y;
   } else {
 #pragma unroll
-    for (int i = 0; i < PER; ++i) f[i] = __bfloat162float(p[i]);
+    for (int i = 0; i < PER; ++i) f[i] = __half2float(p[i]);
   }
 }
 
@@ -194,7 +195,7 @@ __device__ __forceinline__ void load_v(const __nv_bfloat16* p, float (&f)[4]) {
 // K/V rows at kb / vb with the given row strides (global cache or smem copy).
 template <int HD>
 __device__ __forceinline__ void att_chunks(const float (&sq)[MAX_G][HD], const __nv_bfloat16* kb, int kstride,
-                                           const __nv_bfloat16* vb, int vstride, int G, int L, int c_begin,
+                                           const __half* vb, int vstride, int G, int L, int c_begin,
                                            int c_step, int lane, float (&m)[MAX_G], float (&l)[MAX_G],
                                            float (&acc)[MAX_G][HD / 32]) {
   constexpr int PER = HD / 32;
@@ -273,7 +274,7 @@ __device__ __forceinline__ void att_chunks(const float (&sq)[MAX_G][HD], const _
 template <int HD, bool ROW_PER_WARP>
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
-    const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
+    const __half* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
     int T, int H, int KV, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
   constexpr int PER = HD / 32;   // output dims per lane
   lp::pdl_wait();
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_kernel(
   const int G = H / KV;
   const int L = pos[t] + 1;
   const __nv_bfloat16* kb = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
-  const __nv_bfloat16* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+  const __half* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
   __shared__ float sq_all[ROW_PER_WARP ? ATT_WARPS : 1][MAX_G][HD];
   float (&sq)[MAX_G][HD] = sq_all[ROW_PER_WARP ? warp : 0];
   if (ROW_PER_WARP) {
@@ -371,8 +372,17 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+// P V runs in fp16 (P in [0, 1] keeps 3 more mantissa bits than bf16; V is
+// stored fp16 in the cache, exact for its activations' range)
+__device__ __forceinline__ void mma_f16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  const __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
@@ -381,7 +391,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 template <int HD, int NST>
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
-    const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
+    const __half* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
     int T, int H, int KV, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
   constexpr int KS = HD + 8;                 // padded smem row (elements): conflict-free fragments
   constexpr int KSTEPS = HD / 16;            // QK^T k-steps
@@ -431,7 +441,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
         for (int i = 0; i < PER; ++i) acc[g][i] = 0.f;
       }
       const __nv_bfloat16* kb = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
-      const __nv_bfloat16* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+      const __half* vb = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
       att_chunks<HD>(sq, kb, HD, vb, HD, G, pos[t] + 1, 0, 32, lane, m, l, acc);
 #pragma unroll
       for (int g = 0; g < MAX_G; ++g) {
@@ -469,7 +479,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
   const float sl2 = scale * 1.4426950408889634f;  // softmax in base 2
   const int len = s_len;
   const __nv_bfloat16* kg = k_cache + ((int64_t)seq[t0] * KV + kh) * max_len * HD;
-  const __nv_bfloat16* vg = v_cache + ((int64_t)seq[t0] * KV + kh) * max_len * HD;
+  const __half* vg = v_cache + ((int64_t)seq[t0] * KV + kh) * max_len * HD;
   constexpr int V8 = HD / 8;
   using Row = __nv_bfloat16[KS];
   Row* const dynK = reinterpret_cast<Row*>(att_dyn);
@@ -568,8 +578,8 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
         }
         // C fragment of S -> A fragment of P (keys 16 kk .. 16 kk + 15)
         const int kk = nt >> 1, hi = nt & 1;
-        pa[kk][2 * hi] = pack_bf16(pv[0], pv[1]);
-        pa[kk][2 * hi + 1] = pack_bf16(pv[2], pv[3]);
+        pa[kk][2 * hi] = pack_f16(pv[0], pv[1]);
+        pa[kk][2 * hi + 1] = pack_f16(pv[2], pv[3]);
       }
       // O += P V: V fragments (k = keys, n = dims) via ldmatrix.trans
 #pragma unroll
@@ -582,7 +592,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_kernel(
           asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
                        : "=r"(b0), "=r"(b1)
                        : "r"(row_addr + dt * 16));
-          mma_bf16_16816(o[dt], pa[kk], b0, b1);
+          mma_f16_16816(o[dt], pa[kk], b0, b1);
         }
       }
     }
@@ -625,7 +635,7 @@ constexpr int DEC_KEYS = 32;
 template <int HD, int NST>
 __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
     const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_cache,
-    const __nv_bfloat16* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
+    const __half* __restrict__ v_cache, const int32_t* __restrict__ pos, const int32_t* __restrict__ seq,
     int H, int KV, int64_t max_len, float scale, __nv_bfloat16* __restrict__ out) {
   constexpr int KS = HD + 8;
   constexpr int KSTEPS = HD / 16;
@@ -641,7 +651,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
   const int L = pos[t] + 1;
   const int r0 = lane >> 2, cq = (lane & 3) * 2;
   const __nv_bfloat16* kg = k_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
-  const __nv_bfloat16* vg = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
+  const __half* vg = v_cache + ((int64_t)seq[t] * KV + kh) * max_len * HD;
   __nv_bfloat16 (*Kbase)[KS] = reinterpret_cast<__nv_bfloat16 (*)[KS]>(dec_smem) + warp * NST * 2 * DEC_KEYS;
   const int cstep = S * ATT_WARPS * DEC_KEYS;
   const int cstart = (split * ATT_WARPS + warp) * DEC_KEYS;
@@ -758,8 +768,8 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
         lrow[h] += pv[i];
       }
       const int kk = nt >> 1, hi = nt & 1;
-      pa[kk][2 * hi] = pack_bf16(pv[0], pv[1]);
-      pa[kk][2 * hi + 1] = pack_bf16(pv[2], pv[3]);
+      pa[kk][2 * hi] = pack_f16(pv[0], pv[1]);
+      pa[kk][2 * hi + 1] = pack_f16(pv[2], pv[3]);
     }
 #pragma unroll
     for (int kk = 0; kk < DEC_KEYS / 16; ++kk) {
@@ -771,7 +781,7 @@ __global__ void __launch_bounds__(ATT_WARPS * 32) attention_mma_decode_kernel(
         asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
                      : "=r"(b0), "=r"(b1)
                      : "r"(row_addr + dt * 16));
-        mma_bf16_16816(o[dt], pa[kk], b0, b1);
+        mma_f16_16816(o[dt], pa[kk], b0, b1);
       }
     }
     __syncwarp();   // this warp's K/V slice is restaged for its next chunk
@@ -1009,7 +1019,7 @@ int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim,
   const unsigned groups = (unsigned)((n_heads + n_kv + ROPE_HEADS - 1) / ROPE_HEADS);
   LP_CUDA(lp::launch(rope_kv_kernel, dim3((unsigned)T, groups + 1), dim3(ROPE_THREADS), 0, (cudaStream_t)stream, qkv, n_heads, n_kv,
                      head_dim, pos, seq, theta, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
-                     (__nv_bfloat16*)v_cache, max_len));
+                     (__half*)v_cache, max_len));
   return 0;
 }
 
@@ -1019,8 +1029,8 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
   LP_CHECK(q && k_cache && v_cache && pos && seq && out && T > 0, "lp_attention: bad arguments");
   LP_CHECK(n_kv > 0 && n_heads % n_kv == 0 && n_heads / n_kv <= MAX_G, "lp_attention: GQA group > %d", MAX_G);
   LP_CHECK(head_dim % 32 == 0 && head_dim <= 128, "lp_attention: head_dim must be 32..128, multiple of 32");
-  const __nv_bfloat16 *qq = (const __nv_bfloat16*)q, *kk = (const __nv_bfloat16*)k_cache,
-                      *vv = (const __nv_bfloat16*)v_cache;
+  const __nv_bfloat16 *qq = (const __nv_bfloat16*)q, *kk = (const __nv_bfloat16*)k_cache;
+  const __half* vv = (const __half*)v_cache;
   __nv_bfloat16* oo = (__nv_bfloat16*)out;
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 blk(ATT_WARPS * 32);

@@ -107,14 +107,15 @@ def _upload(graph):
 
 
 class KVCache:
-    """bf16 K and V caches per layer: [max_seqs, n_kv, max_len, head_dim]."""
+    """K (bf16) and V (fp16) caches per layer: [max_seqs, n_kv, max_len, head_dim].
+    V is fp16 because attention's P V product runs in fp16 (lp_llama.cu)."""
 
     def __init__(self, cfg, layers, max_seqs: int, max_len: int, device):
         import torch
         self.max_seqs, self.max_len = max_seqs, max_len
         shape = (max_seqs, cfg.n_kv_heads, max_len, cfg.head_dim)
         self.k = {l: torch.zeros(shape, dtype=torch.bfloat16, device=device) for l in layers}
-        self.v = {l: torch.zeros(shape, dtype=torch.bfloat16, device=device) for l in layers}
+        self.v = {l: torch.zeros(shape, dtype=torch.float16, device=device) for l in layers}
 
 
 class LlamaExecutor:

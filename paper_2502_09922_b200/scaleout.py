@@ -250,6 +250,12 @@ class ScaleOut:
         s = stream or torch.cuda.current_stream()
         sp = E.N.stream_ptr(s)
         t0 = time.perf_counter()
+        vnodes = [n for n in self.cluster.exec_nodes if n not in self.plan.sources] if self.verify else []
+        for node in vnodes:     # allocated before ev0: nothing of this run may follow on s and touch them
+            if node not in self._vbuf:
+                self._vbuf[node] = (torch.empty(self.plan.block_count, dtype=torch.int64, device=s.device),
+                                    torch.empty(self.plan.block_count, dtype=torch.int64, pin_memory=True),
+                                    torch.cuda.Stream(device=s.device))
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(s)
         if not self._loaded:
@@ -265,13 +271,8 @@ class ScaleOut:
             epoch = self.launch(sp)
             self.kernel_launches = 1 + int(self.pull_ctas > 0)    # count reset + multicast kernel
         assert epoch == epoch_next
-        vnodes = [n for n in self.cluster.exec_nodes if n not in self.plan.sources] if self.verify else []
         vstreams = []
         for node in vnodes:
-            if node not in self._vbuf:
-                self._vbuf[node] = (torch.zeros(self.plan.block_count, dtype=torch.int64, device=s.device),
-                                    torch.empty(self.plan.block_count, dtype=torch.int64, pin_memory=True),
-                                    torch.cuda.Stream(device=s.device))
             vs = self._vbuf[node][2]
             vs.wait_event(ev0)
             self.cluster.engine.verify(node, epoch, self._vbuf[node][0].data_ptr(), vs.cuda_stream,

@@ -91,7 +91,7 @@ def _check_attention(hd, H, KV, ctx, run, max_len):
     g = torch.Generator(device="cuda").manual_seed(hd + H + len(ctx))
     seqs = len(ctx)
     kc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
-    vc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.float16)
     pos = [c - 1 for c in ctx] + list(range(ctx[0] - 1, max(ctx[0] - run, -1), -1))
     seq = list(range(seqs)) + [0] * (len(pos) - seqs)
     T = len(pos)

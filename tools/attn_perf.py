@@ -18,7 +18,7 @@ P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 def run(H, KV, hd, seqs, ctx, prefill, max_len=None):
     max_len = max_len or ctx + 8
     kc = (torch.randn(seqs, KV, max_len, hd, device="cuda") * 0.5).to(torch.bfloat16)
-    vc = torch.randn(seqs, KV, max_len, hd, device="cuda").to(torch.bfloat16)
+    vc = torch.randn(seqs, KV, max_len, hd, device="cuda").to(torch.float16)
     if prefill:   # every position of every sequence
         pos = torch.arange(ctx, dtype=torch.int32, device="cuda").repeat(seqs)
         seq = torch.arange(seqs, dtype=torch.int32, device="cuda").repeat_interleave(ctx)
