@@ -358,29 +358,35 @@ class Cluster:
                 tile_bytes: int = DEFAULT_TILE):
         """One process driving several GPUs: GPU node i lives on device
         ``node_devices[i]`` (node ids shift by one if a host node 0 exists).
+        An entry of -1 makes that node a HOST node instead (the box's
+        pinned host copy, at any position — e.g. the second source of a
+        tier-driven plan, GPU copies first); several HOST positions share
+        one pinned copy.
         One engine per device holds the full node table; each device runs
         one kernel over its own nodes (peer access enabled both ways)."""
-        devs = sorted(set(node_devices))
+        node_devices = ([-1] if host_node else []) + list(node_devices)
+        devs = sorted(set(d for d in node_devices if d >= 0))
         for a in devs:
             for b in devs:
                 if a != b:
                     N.call("lp_enable_peer", a, b)
-        off = 1 if host_node else 0
-        n_nodes = len(node_devices) + off
+        n_nodes = len(node_devices)
         engines = {}
         for d in devs:
             with on_device(d):
                 engines[d] = MulticastEngine(n_nodes, block_offsets, block_lengths, tile_bytes)
         nodes, host = [], None
-        if host_node:
-            with on_device(devs[0]):
-                host = HostImage(image_bytes)
-            nodes.append(NodeBuffer(0, LP_NODE_HOST, -1, host.device_ptr))
         for i, d in enumerate(node_devices):
+            if d < 0:                       # every HOST position shares the one pinned copy
+                if host is None:
+                    with on_device(devs[0]):
+                        host = HostImage(image_bytes)
+                nodes.append(NodeBuffer(i, LP_NODE_HOST, -1, host.device_ptr))
+                continue
             img = dev_malloc(d, image_bytes)
             sig = dev_malloc(d, engines[d].signal_bytes)
             N.call("lp_memset", C.c_void_p(sig), 0, engines[d].signal_bytes, None)
-            nodes.append(NodeBuffer(i + off, LP_NODE_GPU, d, img, sig, [("dev", img), ("dev", sig)]))
+            nodes.append(NodeBuffer(i, LP_NODE_GPU, d, img, sig, [("dev", img), ("dev", sig)]))
         for d, eng in engines.items():
             for nb in nodes:
                 eng.set_node(nb.node, nb.kind, nb.image, nb.signals)
@@ -586,7 +592,8 @@ def load_source_image(cluster: "Cluster", node: int, layout, seed: int, device: 
         return
     scratch = dev_malloc(device, layout.weights_bytes)
     try:
-        fill_image(scratch, layout, seed)
+        with on_device(device):
+            fill_image(scratch, layout, seed)
         N.call("lp_memcpy", C.c_void_p(cluster.host.host_ptr), C.c_void_p(scratch), layout.weights_bytes,
                None)
         N.call("lp_sync_device", device)

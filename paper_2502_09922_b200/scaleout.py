@@ -7,9 +7,19 @@ groups, execution pipelines with activation steps — then, instead of pushing
 modelled ``transfer_step_done`` events, it executes the schedule with the
 CUDA multicast engine and reports measured times.
 
-Node numbering follows the reference CLI (cli.py:308-309): ``nodes[:k]`` are
-the sources.  On one box a node is a GPU (rank); a HOST node (pinned memory)
-is node 0 when the source tier is host memory (config C3).
+Two entry points:
+
+* :func:`plan_scale_out` — the reference CLI's numbering (cli.py:308-309):
+  ``nodes[:k]`` are the sources; on one box a node is a GPU (rank) and a
+  HOST node (pinned memory) is node 0 when the source tier is host memory
+  (config C3).
+* :func:`plan_from_tiers` / :func:`scale_out` — the simulator's tier-driven
+  sequence (simengine.py:442-467 ``_scale_out`` -> ``startup_plan`` ->
+  ``_warm_and_hot`` -> ``_launch_lambda_scale``): demand nodes are classified
+  hot / warm / cold from a ``TierMap`` (modelmgr.py:109-141), sources are the
+  GPU-resident copies first and then host-memory copies (the box's pinned
+  host copy is one more node, the HOST node), ``k_eff = min(|sources|,
+  |cold|, k)``, and the λPipe plan covers ``sources + cold`` in that order.
 """
 
 from __future__ import annotations
@@ -20,6 +30,7 @@ from dataclasses import dataclass, field
 from . import engine as E
 from .cluster import ClusterSpec, b200_box, transfer_step_time
 from .image import CONFIGS, ImageLayout, LlamaConfig, build_layout, model_spec
+from .modelmgr import COLD, GPU, HOT, MEMORY, WARM, StartupPlan, TierMap, startup_plan
 from .multicast import (MulticastSchedule, SubGroup, Transfer, attach_orders, compose_schedule,
                         k_way_orders, partition_subgroups, schedule_to_lines, select_block_count)
 from .pipeline import assign_blocks_to_stages, completion_ordered_groups, generate_pipelines
@@ -38,6 +49,7 @@ class ScaleOutPlan:
     step_s_model: float
     host_source: bool = False
     strategy: str = "lambda"
+    host_nodes: tuple = ()        # positions that are the HOST node (pinned host copy)
 
     @property
     def block_count(self) -> int:
@@ -92,12 +104,18 @@ def sharded_host_schedule(n_nodes: int, plan) -> MulticastSchedule:
 
 def plan_scale_out(config, n_nodes: int, k: int = 1, block_count="auto",
                    cluster: ClusterSpec | None = None, host_source: bool = False,
-                   strategy: str = "lambda") -> ScaleOutPlan:
+                   strategy: str = "lambda", host_nodes: tuple | None = None) -> ScaleOutPlan:
     """Planning half of ``_launch_lambda_scale`` (simengine.py:579-590).
 
+    ``host_nodes``: positions that are the HOST node (default: node 0 when
+    ``host_source``); a HOST node must be one of the k sources.
     ``strategy="sharded_host"`` (host sources only) replaces the binomial
     schedule by :func:`sharded_host_schedule`; it has no λPipe pipelines
     (every GPU completes at about the same time)."""
+    if host_nodes is None:
+        host_nodes = (0,) if host_source else ()
+    host_nodes = tuple(host_nodes)
+    host_source = bool(host_nodes)
     if strategy not in ("lambda", "sharded_host"):
         raise ValueError("strategy is 'lambda' or 'sharded_host'")
     if strategy == "sharded_host" and not host_source:
@@ -111,6 +129,8 @@ def plan_scale_out(config, n_nodes: int, k: int = 1, block_count="auto",
     nodes = list(range(n_nodes))
     k_eff = max(1, min(k, n_nodes - 1)) if n_nodes > 1 else 1
     sources = nodes[:k_eff]
+    if any(h not in sources for h in host_nodes):
+        raise ValueError("a HOST node must be one of the sources (positions < k)")
     groups = attach_orders(partition_subgroups(nodes, sources), k_way_orders(layout.plan.block_count, k_eff))
     sched = compose_schedule(groups, layout.plan, cluster.step_fixed_overhead_s, cluster.nic_Bps)
     ordered = completion_ordered_groups(groups, sched)
@@ -120,9 +140,103 @@ def plan_scale_out(config, n_nodes: int, k: int = 1, block_count="auto",
     step_s = transfer_step_time(sched, layout.plan, cluster)
     if strategy == "sharded_host":
         sched = sharded_host_schedule(n_nodes, layout.plan)
+        if host_nodes != (0,):
+            raise ValueError("sharded_host needs the HOST node at position 0")
         return ScaleOutPlan(cfg, layout, nodes, [0], list(sched.groups), sched, list(sched.groups), [], step_s,
-                            host_source, strategy)
-    return ScaleOutPlan(cfg, layout, nodes, sources, groups, sched, ordered, eps, step_s, host_source)
+                            host_source, strategy, host_nodes)
+    return ScaleOutPlan(cfg, layout, nodes, sources, groups, sched, ordered, eps, step_s, host_source,
+                        host_nodes=host_nodes)
+
+
+@dataclass
+class TieredPlan:
+    """A tier-driven scale-out (simengine.py:442-467, :507-521, :564-602).
+
+    ``plan`` is the λPipe multicast to the cold nodes over positions
+    0..n-1 (``None`` when nothing is cold); ``ref_nodes[i]`` is the
+    reference node id at position i (the HOST node's id is ``host_id``).
+    Warm demand nodes load locally from host memory (the reference's h2d
+    path, ``warm_loads`` rows (block, node) in block order); hot ones serve
+    at once."""
+    startup: StartupPlan
+    hot: list
+    warm: list
+    cold: list
+    sources: list                 # reference ids, after k_eff
+    plan: ScaleOutPlan | None
+    ref_nodes: list
+    host_id: int | None
+
+    def position(self, ref_node: int) -> int:
+        return self.ref_nodes.index(ref_node)
+
+    def ref_lines(self) -> list:
+        """The multicast schedule in reference node ids (schedule_to_lines format)."""
+        if self.plan is None:
+            return []
+        rows = sorted((t.step, self.ref_nodes[t.sender], self.ref_nodes[t.receiver], t.block_id)
+                      for row in self.plan.schedule.steps for t in row)
+        return [f"{a},{b},{c},{d}" for a, b, c, d in rows]
+
+
+def box_tiers(model_id: str, block_count: int, gpu_resident=(), host_copy: bool = True, host_id: int = 8,
+              warm=()) -> TierMap:
+    """The residency of one model on a B200 box in the reference's terms: GPU
+    node g holds a GPU-tier copy for g in ``gpu_resident``; the box's pinned
+    host copy is node ``host_id`` with a MEMORY-tier copy; nodes in ``warm``
+    hold a node-local MEMORY copy (they load over their own PCIe link)."""
+    tm = TierMap()
+    blocks = set(range(block_count))
+    for g in gpu_resident:
+        tm.ensure(g, model_id).gpu_blocks = set(blocks)
+    if host_copy:
+        tm.ensure(host_id, model_id).mem_blocks = set(blocks)
+    for w in warm:
+        tm.ensure(w, model_id).mem_blocks = set(blocks)
+    return tm
+
+
+def plan_from_tiers(config, demand: list, tiers: TierMap, k: int = 1, block_count: int = 16,
+                    host_id: int | None = None, cluster: ClusterSpec | None = None) -> TieredPlan:
+    """``startup_plan`` -> ``_warm_and_hot`` -> ``_launch_lambda_scale``'s
+    planning on reference node ids (simengine.py:450-452, :507-521, :564-590):
+    classify ``demand``; sources = GPU copies then MEMORY copies (<= k);
+    if every source is itself cold, the first one seeds the rest; ``k_eff =
+    min(|sources|, |cold|, k)``; λPipe over ``sources + cold``.  ``host_id``
+    names the box's pinned host copy when it is a node of its own; every
+    source whose copy is in host memory (that node, or a warm demand node that
+    also loads itself, as in the reference) becomes a HOST position of the
+    plan — on one box they all read the same pinned host copy."""
+    cfg = CONFIGS[config] if isinstance(config, str) else config
+    if not isinstance(block_count, int):
+        raise ValueError("plan_from_tiers needs an explicit block_count")
+    sp = startup_plan(cfg.name, block_count, list(demand), tiers, k_max=k)
+    hot = [n for n in demand if sp.classes[n] == HOT]
+    warm = [n for n in demand if sp.classes[n] == WARM]
+    cold = [n for n in demand if sp.classes[n] == COLD]
+    if not cold:
+        return TieredPlan(sp, hot, warm, cold, [], None, [], host_id)
+    sources = [s for s in sp.sources if s not in cold]
+    if not sources:
+        sources = sp.sources[:1]
+        cold = [n for n in cold if n not in sources]
+        if not cold:
+            return TieredPlan(sp, hot, warm, cold, sources, None, [], host_id)
+    k_eff = min(len(sources), len(cold), k)
+    sources = sources[:k_eff]
+    ref_nodes = sources + cold
+    def tier_of(n):
+        st = tiers.get(n, cfg.name)
+        if st is not None and len(st.gpu_blocks) >= block_count:
+            return GPU
+        if st is not None and len(st.mem_blocks) >= block_count:
+            return MEMORY
+        return None                        # the SSD bootstrap: seeded before the multicast
+    # a source whose copy is in host memory sends from it: on one box every
+    # such source reads the box's one pinned host copy (the HOST node)
+    hosts = tuple(i for i, n in enumerate(sources) if tier_of(n) == MEMORY)
+    plan = plan_scale_out(cfg, len(ref_nodes), k_eff, block_count, cluster=cluster, host_nodes=hosts)
+    return TieredPlan(sp, hot, warm, cold, sources, plan, ref_nodes, host_id)
 
 
 def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
@@ -131,12 +245,12 @@ def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
     direction == 1 (pull) or the sender is the HOST node, else the sender.
     Rows (step, sender, receiver, block, wait) in (step, sender, receiver)
     order; ``wait`` = the sender is not a source (it must first receive)."""
-    host = 0 if plan.host_source else None
+    hosts = set(plan.host_nodes)
     srcs = set(plan.sources)
     rows = sorted((t.step, t.sender, t.receiver, t.block_id) for row in plan.schedule.steps for t in row)
     out = []
     for step, snd, rcv, blk in rows:
-        pulled = direction == 1 or snd == host
+        pulled = direction == 1 or snd in hosts
         if (pulled and rcv == node) or (not pulled and snd == node):
             out.append((step, snd, rcv, blk, int(snd not in srcs)))
     return out
@@ -328,18 +442,125 @@ class ScaleOut:
         self.cluster.close()
 
 
-def scale_out(model, sources, targets, k: int = 1, block_count="auto", host_source: bool = False,
-              distributed: bool = False, **kw):
-    """Drop-in entry: plan + execute one λPipe scale-out.
+class TieredScaleOut:
+    """Executes a :class:`TieredPlan` on this process's GPUs (one process,
+    ``engine.Cluster.devices``): position i of the multicast lives on device
+    ``node_devices[ref_nodes[i]]`` (the HOST node in pinned host memory),
+    warm demand nodes load every block from the host copy over their own
+    PCIe link (copy engine, block order), hot ones keep their copy.  The
+    multicast runs in-kernel in the pull direction (receivers read peers over
+    NVLink and the host over PCIe)."""
 
-    ``sources``/``targets`` are node ids; only the reference's canonical
-    ``nodes = sources + targets`` ordering is supported (cli.py:308-309).
-    Returns ``(ScaleOut, ScaleOutResult)``.
-    """
-    nodes = list(sources) + list(targets)
-    if nodes != list(range(len(nodes))):
-        raise ValueError("scale_out expects sources first, nodes numbered 0..N-1")
-    plan = plan_scale_out(model, len(nodes), k=max(k, 1), block_count=block_count, host_source=host_source)
-    so = ScaleOut(plan, distributed=distributed, **kw)
-    so.load_sources()
-    return so, so.run()
+    def __init__(self, tp: TieredPlan, node_devices: dict | None = None, seed: int = 0,
+                 tile_bytes: int = 1 << 20):
+        self.tp = tp
+        self.seed = seed
+        self.dev_of = dict(node_devices or {})
+        self.cluster = None
+        self.warm_images = {}
+        self.host = None
+        if tp.plan is not None:
+            lay = tp.plan.layout
+            devs = [-1 if i in tp.plan.host_nodes else self.dev_of.get(n, n) for i, n in enumerate(tp.ref_nodes)]
+            self.cluster = E.Cluster.devices(devs, lay.block_offsets, lay.block_lengths, lay.weights_bytes,
+                                             tile_bytes=tile_bytes)
+            self.host = self.cluster.host
+
+    @property
+    def plan(self):
+        return self.tp.plan
+
+    def load_sources(self, layout=None):
+        lay = layout or self.tp.plan.layout
+        self.layout = lay
+        if self.cluster is not None:
+            for i in self.tp.plan.sources:
+                E.load_source_image(self.cluster, i, lay, self.seed, device=self._any_device())
+            self.cluster.set_schedule_all(self.tp.plan.schedule, self.tp.plan.sources)
+        if self.tp.warm:
+            if self.host is None:
+                with E.on_device(self._any_device()):
+                    self.host = E.HostImage(lay.weights_bytes)
+                scratch = E.dev_malloc(self._any_device(), lay.weights_bytes)
+                with E.on_device(self._any_device()):
+                    E.fill_image(scratch, lay, self.seed)
+                    E.N.call("lp_memcpy", E.C.c_void_p(self.host.host_ptr), E.C.c_void_p(scratch),
+                             lay.weights_bytes, None)
+                E.N.call("lp_sync_device", self._any_device())
+                E.dev_free(self._any_device(), scratch)
+            for w in self.tp.warm:
+                d = self.dev_of.get(w, w)
+                self.warm_images[w] = (d, E.dev_malloc(d, lay.weights_bytes))
+
+    def _any_device(self) -> int:
+        return min([self.dev_of.get(n, n) for n in (self.tp.ref_nodes or self.tp.warm or self.tp.hot)
+                    if n != self.tp.host_id] or [0])
+
+    def launch(self, streams: dict, pull_ctas: int = 32) -> int | None:
+        """Start the multicast (one kernel per device on ``streams[device]``)
+        and the warm nodes' host loads; returns the multicast epoch."""
+        import torch
+        lay = self.layout
+        for w, (d, img) in self.warm_images.items():
+            st = streams[d]
+            with torch.cuda.stream(st):
+                for b in range(len(lay.block_offsets)):      # block order (the reference's h2d chunks)
+                    o, n = lay.block_offsets[b], lay.block_lengths[b]
+                    E.N.call("lp_memcpy", E.C.c_void_p(img + o), E.C.c_void_p(self.host.host_ptr + o), n,
+                             E.C.c_void_p(st.cuda_stream))
+        if self.cluster is None:
+            return None
+        return self.cluster.launch_devices(streams, 0, pull_ctas)
+
+    def wait(self, streams: dict):
+        if self.cluster is not None:
+            self.cluster.wait_devices()
+        for st in streams.values():
+            st.synchronize()
+
+    def checksums(self) -> dict:
+        """reference node id -> per-block checksums of every demand node's copy."""
+        lay = self.layout
+        out = {}
+        if self.cluster is not None:
+            for i, n in enumerate(self.tp.ref_nodes):
+                if i in self.tp.plan.sources:
+                    continue
+                nb = self.cluster.node(i)
+                with E.on_device(nb.device):
+                    out[n] = E.block_checksums(nb.image, lay.block_offsets, lay.block_lengths)
+        for w, (d, img) in self.warm_images.items():
+            with E.on_device(d):
+                out[w] = E.block_checksums(img, lay.block_offsets, lay.block_lengths)
+        return out
+
+    def close(self):
+        for w, (d, img) in self.warm_images.items():
+            E.dev_free(d, img)
+        self.warm_images = {}
+        if self.cluster is not None:
+            self.cluster.close()
+            self.cluster = None
+        elif self.host is not None:
+            self.host.close()
+        self.host = None
+
+
+def scale_out(model, demand: list, tiers: TierMap, k: int = 1, block_count: int = 16, host_id: int | None = None,
+              node_devices: dict | None = None, seed: int = 0, pull_ctas: int = 32):
+    """Drop-in entry for the simulator's scale-out of
+    ``demand`` nodes (simengine.py:442-467 then :564-602) on real GPUs:
+    ``startup_plan`` over ``tiers`` (GPU copies first, then the box's host
+    copy ``host_id``), hot nodes kept, warm nodes loaded from host memory,
+    the λPipe multicast to the cold ones executed and waited for.  Returns
+    ``(TieredScaleOut, epoch)``; the caller closes it."""
+    import torch
+    tp = plan_from_tiers(model, demand, tiers, k, block_count, host_id)
+    so = TieredScaleOut(tp, node_devices, seed)
+    so.load_sources(tp.plan.layout if tp.plan is not None else build_layout(
+        CONFIGS[model] if isinstance(model, str) else model, block_count))
+    devs = sorted({so.dev_of.get(n, n) for n in tp.ref_nodes + tp.warm if n != host_id})
+    streams = {d: torch.cuda.Stream(device=d) for d in devs}
+    epoch = so.launch(streams, pull_ctas)
+    so.wait(streams)
+    return so, epoch

@@ -25,7 +25,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 SEED = 7            # image seed the GPU tests and the smoke fill
-GATE = 0.05         # >= 5x the measured max |GPU - bf16 oracle| logit error (tests/test_decoder_gpu.py)
+GATE = 0.1          # >= 2.5x the measured max |GPU - bf16 oracle| logit error (0.038, tests/test_decoder_gpu.py);
+                    # bf16 roundings amplify accumulation-order noise: a 1e-7 weight perturbation moves
+                    # the bf16 oracle's own logits by 0.02 (tests/test_prompts_golden.py)
 STEPS = 16          # generated tokens per prompt
 LENGTHS = (8, 9, 10, 11, 12, 13, 14, 15, 16, 20, 24, 32)
 

@@ -17,7 +17,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 PROMPT, DECODE = 160, 4
-TOL = 0.03          # absolute, logits of std ~1 (bf16 activations; accumulation order differs)
+TOL = 0.05          # absolute, logits of std ~1 (measured 0.025 for 8B, 0.010 for 70B: bf16 rounding points
+                    # amplify accumulation-order differences, tests/test_prompts_golden.py)
 
 
 @pytest.mark.parametrize("name", ["llama3-8b", "llama3-70b"])
