@@ -299,6 +299,9 @@ def run_reference(args):
 # our arm
 
 
+POISON = True
+
+
 def timed_steps(so, steps, warmup, distributed, stream, want=None):
     """Device time per step (max over ranks).  With ``want`` (the source's
     per-block checksums) every step's verify-as-it-lands sums are checked;
@@ -308,7 +311,8 @@ def timed_steps(so, steps, warmup, distributed, stream, want=None):
     import torch.distributed as dist
     times, ok, launches = [], True, 0
     for i in range(warmup + steps):
-        so.poison(0x5A ^ i, stream)      # receivers start every step without the model (untimed)
+        if POISON:
+            so.poison(0x5A ^ i, stream)  # receivers start every step without the model (untimed)
         if distributed:
             dist.barrier()
         torch.cuda.synchronize()
@@ -355,6 +359,7 @@ def main():
                          "binomial schedule; sharded_host is always measured beside it at N >= 2)")
     ap.add_argument("--executor", default="auto", choices=["auto", "hybrid", "kernel", "ce"],
                     help="host-sourced scale-out executor (auto = scaleout.choose_executor)")
+    ap.add_argument("--no-poison", action="store_true", help="A/B only: skip overwriting receivers between steps")
     ap.add_argument("--no-gpu-source", action="store_true")
     ap.add_argument("--no-serving", action="store_true")
     ap.add_argument("--requests", type=int, default=32)
@@ -362,6 +367,8 @@ def main():
     ap.add_argument("--no-serving-70b", action="store_true")
     ap.add_argument("--burst-compress", type=float, default=60.0)
     args = ap.parse_args()
+    global POISON
+    POISON = not args.no_poison
     if args.impl == "reference":
         return run_reference(args)
 
@@ -480,6 +487,7 @@ def main():
 
     # --- execute-while-load serving (tokens/s + TTFT during load) ------------
     serving = None
+    serving_host = None
     serving70 = None
     burst = None
     if distributed and N >= 3 and not args.no_serving:
@@ -497,6 +505,13 @@ def main():
                                    "(cross-device pipelines); other ranks idle at a barrier")
             except Exception as e:  # noqa: BLE001
                 serving = {"error": f"{type(e).__name__}: {e}"}
+            try:   # tier-driven plan: GPU 0 + the pinned host copy as the k = 2 sources
+                serving_host = run_serving(N, model=C2_MODEL, k=2, blocks=C2_BLOCKS, requests=args.requests,
+                                           host_source=True)
+                serving_host["note"] = ("startup_plan sources: GPU 0 (GPU tier) then the pinned host copy "
+                                        "(MEMORY tier); one sub-group and its pipeline stages are fed over PCIe")
+            except Exception as e:  # noqa: BLE001
+                serving_host = {"error": f"{type(e).__name__}: {e}"}
             if N >= 4 and not args.no_serving_70b:
                 # BASELINE configs[3]: Llama-3-70B (141 GB per replica) with λPipe
                 # pipelines over partial replicas while the multicast runs
@@ -601,6 +616,8 @@ def main():
             line["gpu_source"] = gpu_source
         if serving:
             line["execute_while_load"] = serving
+        if serving_host:
+            line["execute_while_load_host_source"] = serving_host
         if serving70:
             line["execute_while_load_70b"] = serving70
         if burst:

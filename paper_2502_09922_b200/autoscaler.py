@@ -13,10 +13,15 @@ persistent packed image + multicast signal area.  A node is
 Every ``eval_interval_s`` the reference rule ``autoscale(policy, queue,
 active + pending)`` (cluster.py, simengine.py:78-92) decides how many
 replicas to add; that many idle GPUs are claimed and a scale-out op is
-planned exactly as ``_launch_lambda_scale`` does (sources = hot nodes, up to
-``k``; ``plan_scale_out``), executed by the multicast engine (copy engines:
-no SM time is taken from serving), with pipelines activating on landed
-blocks and a mode switch at completion (``serving.Server`` machinery).
+planned exactly as ``_scale_out`` / ``_launch_lambda_scale`` do
+(simengine.py:442-467, :564-590): ``startup_plan`` over the box's tiers — hot
+GPUs hold a GPU copy, the optional pinned host copy (``host_copy``, node id
+``len(devices)``) a MEMORY copy, released GPUs lose theirs (the eviction of
+simengine.py:404-416) — picks GPU sources first, then the host copy, up to
+``k``; ``scaleout.plan_from_tiers`` builds the λPipe plan, executed by the
+multicast engine (copy engines: no SM time is taken from serving; host rows
+are PCIe DMA), with pipelines activating on landed blocks and a mode switch
+at completion (``serving.Server`` machinery).
 Events use the reference's kinds so ``workload.aggregate`` yields TTFT
 percentiles, the tokens/s timeline and GPU-seconds.
 """
@@ -30,9 +35,9 @@ from collections import deque
 from . import engine as E
 from .cluster import AutoscalePolicy, autoscale
 from .image import CONFIGS, build_layout, model_spec
-from .multicast import attach_orders, compose_schedule, k_way_orders, partition_subgroups
-from .pipeline import assign_blocks_to_stages, completion_ordered_groups, generate_pipelines, plan_mode_switch
-from .scaleout import CE_TILE
+from .pipeline import plan_mode_switch
+from .modelmgr import TierMap
+from .scaleout import CE_TILE, plan_from_tiers
 from .serving import Request, Server, Stage
 from .workload import SimEvent
 
@@ -69,7 +74,8 @@ class AutoscaleServer(Server):
 
     def __init__(self, model, devices: list, block_count: int = 16, k: int = 1, hot: tuple = (0,),
                  policy: AutoscalePolicy | None = None, local_slots: int = 16, max_len: int = 192,
-                 use_graphs: bool = True, seed: int = 20250815, max_replicas: int | None = None):
+                 use_graphs: bool = True, seed: int = 20250815, max_replicas: int | None = None,
+                 host_copy: bool = False):
         import torch
         self.torch = torch
         self.cfg = CONFIGS[model] if isinstance(model, str) else model
@@ -99,6 +105,18 @@ class AutoscaleServer(Server):
         self.cluster = _Nodes(self.buffers)
         for n in hot:
             E.load_source_image(self.cluster, n, lay, seed)
+        self.host_id = len(devices)          # reference node id of the box's pinned host copy
+        self.host = None
+        if host_copy:
+            with E.on_device(devices[0]):
+                self.host = E.HostImage(lay.weights_bytes)
+            scratch = E.dev_malloc(devices[0], lay.weights_bytes)
+            with E.on_device(devices[0]):
+                E.fill_image(scratch, lay, seed)
+                E.N.call("lp_memcpy", E.C.c_void_p(self.host.host_ptr), E.C.c_void_p(scratch), lay.weights_bytes,
+                         None)
+            E.N.call("lp_sync_device", devices[0])
+            E.dev_free(devices[0], scratch)
         for d in devices:
             torch.cuda.synchronize(d)
         self.state = {n: ("hot" if n in hot else "idle") for n in range(len(devices))}
@@ -113,27 +131,36 @@ class AutoscaleServer(Server):
         self.decisions = []     # (t, queue, active, pending, scale_out, room) per evaluation
 
     # -- scale-out --------------------------------------------------------------
-    def _plan(self, sources, targets):
-        nodes = list(range(len(sources) + len(targets)))
-        srcs = nodes[:len(sources)]
-        groups = attach_orders(partition_subgroups(nodes, srcs), k_way_orders(self.lay.plan.block_count, len(srcs)))
-        sched = compose_schedule(groups, self.lay.plan)
-        ordered = completion_ordered_groups(groups, sched)
-        pipes = generate_pipelines(ordered)
-        eps = [assign_blocks_to_stages(pn, [g.transfer_order for g in ordered], self.lay.plan.block_count, sched, i)
-               for i, pn in enumerate(pipes)]
-        return sched, srcs, eps
+    def tiers(self) -> TierMap:
+        """The box's residency in the reference's terms: serving (hot) GPUs hold
+        a GPU copy, the pinned host copy (node ``host_id``) a MEMORY copy;
+        loading and released GPUs hold nothing usable as a source."""
+        tm = TierMap()
+        blocks = set(range(self.lay.plan.block_count))
+        for n, st in self.state.items():
+            tm.ensure(n, self.cfg.name).gpu_blocks = set(blocks) if st == "hot" else set()
+        if self.host is not None:
+            tm.ensure(self.host_id, self.cfg.name).mem_blocks = set(blocks)
+        return tm
 
     def _scale_out(self, now, want):
         idle = [n for n, st in self.state.items() if st == "idle"]
-        hot = [n for n, st in self.state.items() if st == "hot"]
         targets = idle[:want]
-        if not targets or not hot:
+        if not targets:
             return
-        sources = hot[:max(1, min(self.k, len(hot), len(targets)))]   # k_eff (simengine.py:579-580)
-        sched, srcs, eps = self._plan(sources, targets)
-        g = sources + targets                                          # op-local -> global
-        bufs = [self.buffers[x] for x in g]
+        try:
+            tp = plan_from_tiers(self.cfg, targets, self.tiers(), k=self.k, block_count=self.lay.plan.block_count,
+                                 host_id=self.host_id)
+        except Exception:     # noqa: BLE001  (no copy anywhere: UnsatisfiableScalingError)
+            return
+        if tp.plan is None:
+            return
+        sources, targets = tp.sources, tp.cold
+        g = tp.ref_nodes                                               # op-local -> global
+        sched, srcs, eps = tp.plan.schedule, tp.plan.sources, tp.plan.pipelines
+        host_nb = (E.NodeBuffer(self.host_id, E.LP_NODE_HOST, -1, self.host.device_ptr)
+                   if self.host is not None else None)
+        bufs = [host_nb if i in tp.plan.host_nodes else self.buffers[x] for i, x in enumerate(g)]
         for x in targets:
             with E.on_device(self.buffers[x].device):
                 E.N.call("lp_memset", E.C.c_void_p(self.buffers[x].signals), 0, self._sig_bytes(), None)
@@ -164,7 +191,8 @@ class AutoscaleServer(Server):
         streams = {d: self.streams[d] for d in cl.per_device}
         op.epoch = cl.launch_devices_ce(streams)
         self.ops.append(op)
-        self.log(now, "scale_out", model=self.cfg.name, nodes=targets, sources=sources, strategy="lambda_scale")
+        self.log(now, "scale_out", model=self.cfg.name, nodes=targets, sources=sources, strategy="lambda_scale",
+                 classes={n: tp.startup.classes[n] for n in targets})
         self._sample_alloc(now)
 
     def _sig_bytes(self):
@@ -315,6 +343,9 @@ class AutoscaleServer(Server):
         return self.events
 
     def close(self):
+        if self.host is not None:
+            self.host.close()
+            self.host = None
         for nb in self.buffers:
             for kind, ptr in nb.owned:
                 E.dev_free(nb.device, ptr)

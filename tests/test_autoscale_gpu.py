@@ -34,3 +34,36 @@ def test_autoscale_burst_tiny():
         assert compared == 12 * len(ids)
     finally:
         srv.close()
+
+
+def test_autoscale_from_host_copy_tiers():
+    """No GPU holds the model at start, only the box's pinned host copy: the
+    first scale-out's startup plan picks the host copy as its (MEMORY-tier)
+    source; later ones use the then-hot GPUs first and the host copy after
+    them (k = 2).  Every token of every request equals the oracle's."""
+    from paper_2502_09922_b200.autoscaler import AutoscaleServer
+    from paper_2502_09922_b200.cluster import AutoscalePolicy
+    from paper_2502_09922_b200.workload import TraceRecord, aggregate
+    from parity import assert_tokens, entries
+
+    policy = AutoscalePolicy(threshold_hi=1.0, keep_alive_s=5.0, min_replicas=0, capacity_per_replica=2,
+                             eval_interval_s=0.01)
+    srv = AutoscaleServer("tiny", [0, 0, 0], block_count=4, k=2, hot=(), policy=policy, local_slots=2,
+                          max_len=64, seed=7, host_copy=True)
+    try:
+        ids = [f"r{i}" for i in range(4)] + [f"s{i}" for i in range(12)]
+        es = dict(zip(ids, entries(len(ids), max_prompt=32)))
+        prompts = {rid: e["prompt"] for rid, e in es.items()}
+        trace = [TraceRecord(rid, 0.0 if rid[0] == "r" else 0.8, "tiny", len(prompts[rid]), 12) for rid in ids]
+        ev = srv.run(trace, prompts, timeout_s=60)
+        outs = [e for e in ev if e.kind == "scale_out"]
+        assert outs and outs[0].payload["sources"] == [srv.host_id], outs[0].payload
+        assert all(c == "cold" for c in outs[0].payload["classes"].values())
+        if len(outs) > 1:           # GPU copies rank ahead of the host copy
+            assert outs[1].payload["sources"][0] != srv.host_id
+        rep = aggregate(ev, "t")
+        assert rep.requests_completed == len(trace)
+        compared = sum(assert_tokens(srv.requests[rid].out, es[rid], 12, what=f"autoscale {rid}") for rid in ids)
+        assert compared == 12 * len(ids)
+    finally:
+        srv.close()

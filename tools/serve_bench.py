@@ -20,7 +20,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int = 16, requests: int = 16,
                 prompt_len: int = 128, out_tokens: int = 32, spacing_s: float = 0.001, pull_ctas: int = 32,
                 local_slots: int = 16, seed: int = 20250815, executor: str = "ce", outdir: str | None = None,
-                node_devices: list | None = None):
+                node_devices: list | None = None, host_source: bool = False):
+    """host_source: the tier-driven plan (scaleout.plan_from_tiers) with GPU 0
+    holding the model and the box's pinned host copy as the second source
+    (k = 2): one sub-group is fed over PCIe, GPUs 1..n-1 are cold."""
     import numpy as np
     import torch
 
@@ -32,9 +35,14 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
     # node_devices: schedule node i on GPU node_devices[i] (default one node per
     # GPU); e.g. 8 nodes on 4 GPUs exercises the 8-node plan on a 4-GPU box
     node_devices = list(node_devices) if node_devices else list(range(n_gpus))
-    n_nodes = len(node_devices)
-    devs = sorted(set(node_devices))
-    plan = SO.plan_scale_out(model, n_nodes, k=k, block_count=blocks)
+    if host_source:
+        tm = SO.box_tiers(model, blocks, gpu_resident=(0,), host_copy=True, host_id=n_gpus)
+        tp = SO.plan_from_tiers(model, list(range(1, n_gpus)), tm, k=k, block_count=blocks, host_id=n_gpus)
+        plan = tp.plan
+        node_devices = [-1 if i in plan.host_nodes else n for i, n in enumerate(tp.ref_nodes)]
+    else:
+        plan = SO.plan_scale_out(model, len(node_devices), k=k, block_count=blocks)
+    devs = sorted(set(d for d in node_devices if d >= 0))
     lay = plan.layout
     tile = SO.CE_TILE if executor == "ce" else 2 << 20
     cl = E.Cluster.devices(node_devices, lay.block_offsets, lay.block_lengths, lay.weights_bytes,
@@ -83,7 +91,8 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
                 print("iter t=%.4f enq=%.4f dev=%.4f tokens=%d batches=%d" % row, file=sys.stderr)
         return {
             "multicast_executor": executor + (" (push direction: one process drives every GPU, DESIGN §5.1)" if executor == "ce" else ""),
-            "workload": f"{model} bf16, GPU sources {plan.sources}, receivers {plan.receivers}, b={blocks}, k={k}; "
+            "workload": f"{model} bf16, sources {plan.sources} (HOST positions {list(plan.host_nodes)}), "
+                        f"receivers {plan.receivers}, b={blocks}, k={k}; "
                         f"{requests} requests x (prompt {prompt_len}, out {out_tokens}), {spacing_s * 1e3:.0f} ms apart at t=0",
             "pipelines": [[(st.node, st.block_lo, st.block_hi) for st in ep.stages] for ep in plan.pipelines],
             "pipeline_activation_s": sorted(srv2.activation_s.values()),
@@ -114,7 +123,9 @@ if __name__ == "__main__":
     ap.add_argument("--pull-ctas", type=int, default=32)
     ap.add_argument("--outdir", default=None, help="write the reference's result files (cli.py:268-281) here")
     ap.add_argument("--node-devices", default="", help="comma list: GPU of each schedule node (default 0..gpus-1)")
+    ap.add_argument("--host-source", action="store_true", help="GPU 0 + the pinned host copy as the k = 2 sources")
     a = ap.parse_args()
     print(json.dumps(run_serving(a.gpus, a.model, a.k, a.blocks, a.requests, out_tokens=a.out_tokens,
                                  executor=a.executor, pull_ctas=a.pull_ctas, outdir=a.outdir,
-                                 node_devices=[int(x) for x in a.node_devices.split(",")] if a.node_devices else None)))
+                                 node_devices=[int(x) for x in a.node_devices.split(",")] if a.node_devices else None,
+                                 host_source=a.host_source)))
