@@ -117,6 +117,12 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 bool pdl_enabled();   // lp_set_pdl(1) and env LP_PDL != 0
 
+// tcgen05 prefill attention (lp_attn_tc.cu): 0 = launched, 1 = shape not
+// covered (use another kernel), < 0 = error
+int attention_tc(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos, const int32_t* seq,
+                 int64_t T, int n_heads, int n_kv, int head_dim, int64_t max_len, float scale, void* out,
+                 cudaStream_t s);
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                    Args&&... args) {

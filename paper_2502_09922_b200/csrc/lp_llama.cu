@@ -1038,6 +1038,16 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
   // (decode): a CTA per row with warps splitting the keys
   const bool many = T * n_kv >= 1024;
   if (many && (head_dim == 64 || head_dim == 128)) {
+    // tcgen05 / TMEM kernel (lp_attn_tc.cu); LP_ATTN_TC=0 keeps the mma.sync one
+    static const int tc_env = [] {
+      const char* e = getenv("LP_ATTN_TC");
+      return e ? atoi(e) : 1;
+    }();
+    if (tc_env) {
+      const int r = lp::attention_tc(q, k_cache, v_cache, pos, seq, T, n_heads, n_kv, head_dim, max_len, scale,
+                                     out, s);
+      if (r <= 0) return r;
+    }
     const int G = n_heads / n_kv;
     const dim3 mgrid((unsigned)((T + MMA_ROWS - 1) / MMA_ROWS), (unsigned)n_kv,
                      (unsigned)((G + ATT_WARPS - 1) / ATT_WARPS));

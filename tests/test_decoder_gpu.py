@@ -213,3 +213,41 @@ def test_generate_api_matches_oracle(tiny):
     outs = generate(ex, [e["prompt"] for e in es], 16)
     compared = sum(assert_tokens(got, e, what=f"generate prompt {len(e['prompt'])}") for got, e in zip(outs, es))
     assert compared == 48
+
+
+@pytest.mark.parametrize("hd,H,KV,lens", [(128, 32, 8, [1024]), (128, 64, 8, [700, 300]), (128, 8, 8, [517]),
+                                           (64, 4, 2, [600, 1, 33]), (128, 32, 8, [64] * 9 + [130])])
+def test_prefill_attention_tcgen05_causal(hd, H, KV, lens):
+    """Prompts laid out as consecutive rows (the serving layout: one or more
+    sequences back to back, positions 0..len-1) through the tcgen05/TMEM
+    prefill kernel (lp_attn_tc.cu), vs a torch fp32 causal softmax over the
+    same bf16 K / fp16 V caches."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(sum(lens) + hd + H)
+    seqs, max_len = len(lens), max(lens) + 16
+    kc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.float16)
+    pos = [p for n in lens for p in range(n)]
+    seq = [s for s, n in enumerate(lens) for _ in range(n)]
+    T = len(pos)
+    assert T * KV >= 1024
+    q = torch.randn(T, H, hd, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.empty(T, H, hd, dtype=torch.bfloat16, device="cuda")
+    p_t = torch.tensor(pos, dtype=torch.int32, device="cuda")
+    s_t = torch.tensor(seq, dtype=torch.int32, device="cuda")
+    scale = 1.0 / math.sqrt(hd)
+    N.check(N.lib().lp_attention(_ptr(q), _ptr(kc), _ptr(vc), _ptr(p_t), _ptr(s_t), T, H, KV, hd, max_len,
+                                 N.C.c_float(scale), _ptr(out), None))
+    torch.cuda.synchronize()
+    G = H // KV
+    row = 0
+    for s, n in enumerate(lens):
+        k = kc[s, :, :n].float().repeat_interleave(G, 0)            # [H, n, hd]
+        v = vc[s, :, :n].float().repeat_interleave(G, 0)
+        qs = q[row:row + n].float().transpose(0, 1) * scale           # [H, n, hd]
+        att = torch.einsum("hid,hjd->hij", qs, k)
+        att = att.masked_fill(torch.ones(n, n, device="cuda", dtype=torch.bool).triu(1), float("-inf"))
+        ref = torch.einsum("hij,hjd->hid", att.softmax(-1), v).transpose(0, 1)
+        err = (out[row:row + n].float() - ref).abs().max().item()
+        assert err < 2e-2, (s, n, err)
+        row += n
