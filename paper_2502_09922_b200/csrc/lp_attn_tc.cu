@@ -22,7 +22,7 @@
 //
 //   warp 0   : TMA producer (Q once, then K/V chunks)
 //   warp 1   : TMEM allocator + MMA issuer (one thread)
-//   warps 2-5: softmax / output (thread = one TMEM lane = one row)
+//   warps 2-9: softmax / output (two threads per row: key / dim halves)
 //
 // A tile whose tokens belong to several sequences (ragged batches) walks the
 // chunks of each sequence run in turn with the other rows masked.
@@ -33,7 +33,7 @@ namespace {
 
 constexpr int TC_M = 128;       // rows per tile (TMEM lanes)
 constexpr int TC_KEYS = 128;    // keys per chunk
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 352;   // warp 0 TMA (Q, K), warp 1 MMA, warps 2-9 softmax, warp 10 TMA (V)
 constexpr int ATOM = TC_M * 128;   // bytes of one 128-row x 128-byte swizzle column block
 
 template <int HD>
@@ -112,11 +112,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   using C = TcCfg<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_empty[2], p_full[2], o_full[2],
+  __shared__ __align__(8) uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_empty[2], p_full[2], o_full[2],
       o_empty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ int s_pos[TC_M], s_seq[TC_M], s_run_of[TC_M];
-  __shared__ int s_run_seq[TC_M], s_run_chunks[TC_M], s_nrun;
+  __shared__ int s_pos[TC_M];                 // per token of the tile (-1 past T)
+  __shared__ int16_t s_seq[TC_M];
+  __shared__ float s_mx[2][TC_M];              // row max / row sum exchange between column halves
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = gridDim.x - 1 - blockIdx.x;          // later (longer) tiles first: causal balance
   const int kh = blockIdx.y;
@@ -125,13 +126,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) {
     lp::mbar_init(&q_full, 1);
     for (int b = 0; b < 2; ++b) {
-      lp::mbar_init(&kv_full[b], 1);
-      lp::mbar_init(&kv_empty[b], 1);
+      lp::mbar_init(&k_full[b], 1);
+      lp::mbar_init(&k_empty[b], 1);
+      lp::mbar_init(&v_full[b], 1);
+      lp::mbar_init(&v_empty[b], 1);
       lp::mbar_init(&s_full[b], 1);
-      lp::mbar_init(&s_empty[b], 4);
-      lp::mbar_init(&p_full[b], 4);
+      lp::mbar_init(&s_empty[b], 8);
+      lp::mbar_init(&p_full[b], 8);
       lp::mbar_init(&o_full[b], 1);
-      lp::mbar_init(&o_empty[b], 4);
+      lp::mbar_init(&o_empty[b], 8);
     }
     lp::fence_mbar_init();
   }
@@ -152,57 +155,51 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   for (int i = threadIdx.x; i < a.R; i += blockDim.x) {
     const bool v = t0 + i < a.T;
     s_pos[i] = v ? a.pos[t0 + i] : -1;
-    s_seq[i] = v ? a.seq[t0 + i] : -1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int i = 0; i < a.R; ++i) {
-      if (s_seq[i] < 0) {
-        s_run_of[i] = -1;
-        continue;
-      }
-      if (n == 0 || s_run_seq[n - 1] != s_seq[i] || s_run_of[i - 1] != n - 1) {
-        s_run_seq[n] = s_seq[i];
-        s_run_chunks[n] = 0;
-        ++n;
-      }
-      s_run_of[i] = n - 1;
-      const int need = (s_pos[i] + TC_KEYS) / TC_KEYS;   // chunks covering keys 0..pos
-      if (need > s_run_chunks[n - 1]) s_run_chunks[n - 1] = need;
-    }
-    s_nrun = n;
+    s_seq[i] = v ? (int16_t)a.seq[t0 + i] : (int16_t)-1;
   }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = tmem_base;
-  const int nrun = s_nrun;
+  // runs of consecutive tokens of one sequence; every role walks them with
+  // run(): [lo, hi) tokens, sequence, chunks covering keys 0..max pos
+  auto run = [&](int lo, int& hi, int& sq, int& chunks) {
+    sq = s_seq[lo];
+    chunks = 0;
+    for (hi = lo; hi < a.R && s_seq[hi] == sq; ++hi) chunks = max(chunks, (s_pos[hi] + TC_KEYS) / TC_KEYS);
+  };
+  const int nvalid = min(a.R, a.T - t0);
 
-  if (warp == 0) {
-    if (lane == 0 && nrun > 0) {
-      // ---------------- TMA producer ----------------
-      lp::mbar_expect_tx(&q_full, C::Q_BYTES);
-      for (int at = 0; at < C::ATOMS; ++at)
-        tma3d(sm + C::OFF_Q + at * ATOM, &tmQ, &q_full, at * 64, kh * a.G, t0);
+  if (warp == 0 || warp == 10) {
+    if (lane == 0) {
+      // ---------------- TMA producers: warp 0 Q + K, warp 10 V ----------------
+      // K_j's stage frees when S_j is done, V_j's when P_j V_j is: separate
+      // rings let K_{j+2} stream in while chunk j is still in softmax / P V
+      const bool is_k = warp == 0;
+      if (is_k) {
+        lp::mbar_expect_tx(&q_full, C::Q_BYTES);
+        for (int at = 0; at < C::ATOMS; ++at)
+          tma3d(sm + C::OFF_Q + at * ATOM, &tmQ, &q_full, at * 64, kh * a.G, t0);
+      }
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      const CUtensorMap* map = is_k ? &tmK : &tmV;
+      uint8_t* base = sm + (is_k ? C::OFF_K : C::OFF_V);
       int it = 0;
-      for (int ri = 0; ri < nrun; ++ri) {
-        const int row = s_run_seq[ri] * a.KV + kh;
-        for (int c = 0; c < s_run_chunks[ri]; ++c, ++it) {
+      for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+        run(lo, hi, sq, nch);
+        const int row = sq * a.KV + kh;
+        for (int c = 0; c < nch; ++c, ++it) {
           const int st = it & 1;
-          if (it >= 2) lp::mbar_wait(&kv_empty[st], ((it >> 1) - 1) & 1);
-          lp::mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
-          for (int at = 0; at < C::ATOMS; ++at) {
-            tma3d(sm + C::OFF_K + st * C::KV_BYTES + at * (TC_KEYS * 128), &tmK, &kv_full[st], at * 64,
-                  c * TC_KEYS, row);
-            tma3d(sm + C::OFF_V + st * C::KV_BYTES + at * (TC_KEYS * 128), &tmV, &kv_full[st], at * 64,
-                  c * TC_KEYS, row);
-          }
+          if (it >= 2) lp::mbar_wait(&empty[st], ((it >> 1) - 1) & 1);
+          lp::mbar_expect_tx(&full[st], C::KV_BYTES);
+          for (int at = 0; at < C::ATOMS; ++at)
+            tma3d(base + st * C::KV_BYTES + at * (TC_KEYS * 128), map, &full[st], at * 64, c * TC_KEYS, row);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && nrun > 0) {
+    if (lane == 0) {
       // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_KEYS >> 3) << 17) |
                                    ((uint32_t)(TC_M >> 4) << 24);          // bf16 x bf16, both K-major
@@ -210,10 +207,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                     ((uint32_t)(TC_M >> 4) << 24);         // fp16 x fp16, B MN-major
       const uint32_t sq = lp::smem_u32(sm + C::OFF_Q);
       int total = 0;
-      for (int ri = 0; ri < nrun; ++ri) total += s_run_chunks[ri];
+      for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+        run(lo, hi, sq, nch);
+        total += nch;
+      }
       auto issue_pv = [&](int j) {
         const int b = j & 1;
         lp::mbar_wait(&p_full[b], (j >> 1) & 1);
+        lp::mbar_wait(&v_full[b], (j >> 1) & 1);
         if (j >= 2) lp::mbar_wait(&o_empty[b], ((j >> 1) - 1) & 1);
         fence_after();
         const uint32_t sp = lp::smem_u32(sm + C::OFF_P + b * C::P_BYTES);
@@ -223,12 +224,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           umma(tmem + C::O_COL + b * HD, desc_sw128(sp + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
                desc_sw128(sv + kk * 2048, TC_KEYS * 128, 1024), idesc_pv, kk > 0);
         commit(&o_full[b]);
-        commit(&kv_empty[b]);     // K_j (S_j done earlier) and V_j are free
+        commit(&v_empty[b]);
       };
       lp::mbar_wait(&q_full, 0);
       for (int it = 0; it < total; ++it) {
         const int st = it & 1;
-        lp::mbar_wait(&kv_full[st], (it >> 1) & 1);
+        lp::mbar_wait(&k_full[st], (it >> 1) & 1);
         if (it >= 2) lp::mbar_wait(&s_empty[st], ((it >> 1) - 1) & 1);
         fence_after();
         const uint32_t sk = lp::smem_u32(sm + C::OFF_K + st * C::KV_BYTES);
@@ -237,107 +238,125 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           umma(tmem + C::S_COL + st * TC_KEYS, desc_sw128(sq + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
                desc_sw128(sk + (kk >> 2) * (TC_KEYS * 128) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
         commit(&s_full[st]);
+        commit(&k_empty[st]);
         if (it > 0) issue_pv(it - 1);
       }
       if (total > 0) issue_pv(total - 1);
     }
-  } else {
-    // ---------------- softmax / output: thread = row ----------------
+  } else if (warp <= 9) {
+    // ---------------- softmax / output ----------------
+    // two warps per TMEM lane quarter: thread (row r, half h) owns keys
+    // [64h, 64h + 64) of every S chunk (= P atom h) and output dims
+    // [h HD/2, (h + 1) HD/2); the row max is exchanged through smem once per
+    // chunk (named barrier over the 256 softmax threads), the row sums only
+    // at the end (both halves scale by the same max).
+    constexpr int HH = HD / 2;
     const int quarter = warp & 3;
+    const int h = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const int i = r / a.G, g = r % a.G;
-    const int prow = i < a.R ? s_pos[i] : -1;
-    const int myrun = i < a.R ? s_run_of[i] : -1;
+    const int prow = i < nvalid ? s_pos[i] : -1;
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    float o[HD];
+    float o[HH];
 #pragma unroll
-    for (int d = 0; d < HD; ++d) o[d] = 0.f;
+    for (int d = 0; d < HH; ++d) o[d] = 0.f;
     float m_run = -INFINITY, l_run = 0.f, m_acc = -INFINITY;
-    float m_hist[2] = {-INFINITY, -INFINITY};
+    float m_h0 = -INFINITY, m_h1 = -INFINITY;    // max used for P of the last even / odd chunk
     auto merge = [&](int j) {
       const int b = j & 1;
       lp::mbar_wait(&o_full[b], (j >> 1) & 1);
       fence_after();
-      const float mj = m_hist[b];
+      const float mj = b ? m_h1 : m_h0;
       const float sc = m_acc == -INFINITY ? 0.f : exp2f(m_acc - mj);
+      uint32_t v[HH];
 #pragma unroll
-      for (int cg = 0; cg < HD / 32; ++cg) {
-        uint32_t v[32];
-        ld32(trow + C::O_COL + b * HD + cg * 32, v);
-        wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) o[cg * 32 + e] = o[cg * 32 + e] * sc + __uint_as_float(v[e]);
-      }
+      for (int cg = 0; cg < HH / 32; ++cg)
+        ld32(trow + C::O_COL + b * HD + h * HH + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cg * 32));
+      wait_ld();
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[b]);
+#pragma unroll
+      for (int e = 0; e < HH; ++e) o[e] = fmaf(o[e], sc, __uint_as_float(v[e]));
       m_acc = mj;
     };
     int it = 0;
-    for (int ri = 0; ri < nrun; ++ri) {
-      const bool mine = myrun == ri;
-      for (int c = 0; c < s_run_chunks[ri]; ++c, ++it) {
+    for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+      run(lo, hi, sq, nch);
+      const bool mine = i >= lo && i < hi;
+      for (int c = 0; c < nch; ++c, ++it) {
         const int b = it & 1;
         lp::mbar_wait(&s_full[b], (it >> 1) & 1);
         fence_after();
-        const int lim = mine ? prow - c * TC_KEYS : -1;     // keys 0..lim of this chunk are visible
-        float cmax = -INFINITY;
-#pragma unroll
-        for (int cg = 0; cg < TC_KEYS / 32; ++cg) {
-          uint32_t v[32];
-          ld32(trow + C::S_COL + b * TC_KEYS + cg * 32, v);
-          wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (cg * 32 + e <= lim) cmax = fmaxf(cmax, __uint_as_float(v[e]) * a.sl2);
-        }
-        const float m_new = fmaxf(m_run, cmax);
-        float lsum = 0.f;
-        uint8_t* prow_s = sm + C::OFF_P + b * C::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-        for (int cg = 0; cg < TC_KEYS / 32; ++cg) {
-          uint32_t v[32];
-          ld32(trow + C::S_COL + b * TC_KEYS + cg * 32, v);
-          wait_ld();
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const int k = cg * 32 + e;
-            const float p0 = (k <= lim) ? exp2f(__uint_as_float(v[e]) * a.sl2 - m_new) : 0.f;
-            const float p1 = (k + 1 <= lim) ? exp2f(__uint_as_float(v[e + 1]) * a.sl2 - m_new) : 0.f;
-            const __half2 h = __floats2half2_rn(p0, p1);
-            const float2 hf = __half22float2(h);
-            lsum += hf.x + hf.y;                       // the fp16 values P V multiplies
-            pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&h);
-          }
-          uint8_t* atom = prow_s + (cg >> 1) * ATOM;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int chunk = ((cg & 1) * 4 + q) ^ (r & 7);
-            *reinterpret_cast<uint4*>(atom + chunk * 16) =
-                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          }
-        }
+        const int lim = mine ? prow - c * TC_KEYS - h * 64 : -1;   // my keys 0..lim are visible
+        uint32_t v[64];
+        ld32(trow + C::S_COL + b * TC_KEYS + h * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+        ld32(trow + C::S_COL + b * TC_KEYS + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        wait_ld();
         fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[b]);   // S buffer b may be overwritten (S_{it+2})
+        // raw scores; the scale (> 0) is applied to the max and inside the exp FFMA
+        float cmax = -INFINITY;
+        if (lim >= 63) {                             // whole half below the diagonal: no mask
+#pragma unroll
+          for (int e = 0; e < 64; ++e) cmax = fmaxf(cmax, __uint_as_float(v[e]));
+        } else if (lim >= 0) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (e <= lim) cmax = fmaxf(cmax, __uint_as_float(v[e]));
+        }
+        cmax *= a.sl2;
+        asm volatile("bar.sync 1, 256;" ::: "memory");   // previous chunk's partner max has been read
+        s_mx[h][r] = cmax;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const float m_new = fmaxf(m_run, fmaxf(cmax, s_mx[h ^ 1][r]));
+        float lsum = 0.f;
+        uint8_t* prow_s = sm + C::OFF_P + b * C::P_BYTES + h * ATOM + (r >> 3) * 1024 + (r & 7) * 128;
+        if (lim < 0) {                               // nothing visible: P = 0
+#pragma unroll
+          for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(prow_s + q * 16) = make_uint4(0, 0, 0, 0);
+        } else {
+          const float nm = -m_new;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {               // 8 x 16 B: keys 8q .. 8q + 7 of my 64
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const int k = q * 8 + e;
+              float p0 = exp2f(fmaf(__uint_as_float(v[k]), a.sl2, nm));
+              float p1 = exp2f(fmaf(__uint_as_float(v[k + 1]), a.sl2, nm));
+              if (lim < 63) {
+                p0 = k <= lim ? p0 : 0.f;
+                p1 = k + 1 <= lim ? p1 : 0.f;
+              }
+              lsum += p0 + p1;
+              const __half2 hv = __floats2half2_rn(p0, p1);
+              pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+            }
+            *reinterpret_cast<uint4*>(prow_s + ((q ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P stores -> visible to the MMA
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&s_empty[b]);
-          mbar_arrive(&p_full[b]);
-        }
+        if (lane == 0) mbar_arrive(&p_full[b]);
         const float al = m_run == -INFINITY ? 0.f : exp2f(m_run - m_new);
-        l_run = l_run * al + lsum;
+        l_run = fmaf(l_run, al, lsum);
         m_run = m_new;
-        m_hist[b] = m_new;
+        if (b) m_h1 = m_new; else m_h0 = m_new;
         if (it > 0) merge(it - 1);
       }
     }
     if (it > 0) merge(it - 1);
-    if (i < a.R && t0 + i < a.T && l_run > 0.f) {
-      const float inv = 1.0f / l_run;
-      __nv_bfloat16* orow = a.out + ((int64_t)(t0 + i) * a.H + kh * a.G + g) * HD;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    s_mx[h][r] = l_run;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float l_tot = l_run + s_mx[h ^ 1][r];
+    if (i < a.R && t0 + i < a.T && l_tot > 0.f) {
+      const float inv = 1.0f / l_tot;
+      __nv_bfloat16* orow = a.out + ((int64_t)(t0 + i) * a.H + kh * a.G + g) * HD + h * HH;
 #pragma unroll
-      for (int d = 0; d < HD; d += 8) {
+      for (int d = 0; d < HH; d += 8) {
         __nv_bfloat162 w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) w[e] = __floats2bfloat162_rn(o[d + 2 * e] * inv, o[d + 2 * e + 1] * inv);

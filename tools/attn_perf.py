@@ -35,14 +35,15 @@ def run(H, KV, hd, seqs, ctx, prefill, max_len=None):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(200):
+    for _ in range(int(os.environ.get("ATTN_ITERS", 200))):
         f()
     e1.record()
     torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) / 200 * 1e3
+    us = e0.elapsed_time(e1) / int(os.environ.get("ATTN_ITERS", 200)) * 1e3
     kv_bytes = (seqs * KV * ctx * hd * 2 * 2) if not prefill else seqs * KV * ctx * hd * 2 * 2
+    flops = 4.0 * hd * H * seqs * ctx * (ctx + 1) / 2 if prefill else 4.0 * hd * H * seqs * ctx
     print(f"{'prefill' if prefill else 'decode '} H={H} KV={KV} seqs={seqs:3d} ctx={ctx:5d} max_len={max_len:5d} rows={T:6d}: "
-          f"{us:8.1f} us  (K/V {kv_bytes / us / 1e3:7.1f} GB/s)", flush=True)
+          f"{us:8.1f} us  (K/V {kv_bytes / us / 1e3:7.1f} GB/s, {flops / us / 1e6:7.1f} TFLOP/s causal)", flush=True)
 
 
 if len(sys.argv) > 1 and sys.argv[1] == "one":     # one decode config (ncu target): one SEQS CTX [MAX_LEN]
@@ -52,6 +53,15 @@ if len(sys.argv) > 1 and sys.argv[1] == "split":   # decode rows vs the cluster 
     for H, KV in ((32, 8), (64, 8)):
         for seqs, ctx in ((16, 160), (16, 1024), (16, 2000), (8, 160), (8, 2000), (4, 2000), (32, 1024), (1, 160)):
             run(H, KV, 128, seqs, ctx, False, 2048)
+    sys.exit(0)
+
+if len(sys.argv) > 1 and sys.argv[1] == "pone":      # one prefill config (ncu target): pone H KV SEQS CTX
+    run(int(sys.argv[2]), int(sys.argv[3]), 128, int(sys.argv[4]), int(sys.argv[5]), True)
+    sys.exit(0)
+if len(sys.argv) > 1 and sys.argv[1] == "prefill":   # prefill only (LP_ATTN_TC=0/1 A/B)
+    for H, KV in ((32, 8), (64, 8), (40, 40)):
+        for seqs, ctx in ((16, 128), (8, 512), (1, 2048), (2, 4096)):
+            run(H, KV, 128, seqs, ctx, True)
     sys.exit(0)
 
 for H, KV in ((32, 8), (64, 8)):
