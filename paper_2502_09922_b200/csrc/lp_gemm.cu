@@ -524,12 +524,17 @@ struct Cfg2 {
   // SwiGLU epilogue transpose tiles: per epilogue warp 32 tokens x 32 rows
   // bf16, rows padded to 80 B (conflict-free 16-byte reads)
   static constexpr int XPOSE_PITCH = 40;                      // bf16 elements per token row
-  static constexpr int XPOSE_BYTES = (EPI == EPI_SWIGLU) ? 4 * 32 * XPOSE_PITCH * 2 : 0;
+  static constexpr int XPOSE_BYTES = (EPI == EPI_SWIGLU) ? 8 * 32 * XPOSE_PITCH * 2 : 0;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + XPOSE_BYTES;
 };
 
+// 8 epilogue warps (two per TMEM lane quarter, alternating 32-token chunks):
+// the single-buffered SwiGLU accumulator's drain is on the critical path, and
+// one warp per SM sub-partition could not hide its TMEM-load and exp latency
+constexpr int PAIR_THREADS = 320;
+
 template <int BT, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmW2,
                      const __grid_constant__ CUtensorMap tmXh, const GemmArgs args) {
   using C = Cfg2<BT, EPI>;
@@ -554,7 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       lp::mbar_init(&tfull[a], 1);
-      lp::mbar_init(&tempty[a], 8);     // 4 epilogue warps x 2 CTAs
+      lp::mbar_init(&tempty[a], 16);    // 8 epilogue warps x 2 CTAs
     }
     lp::fence_mbar_init();
   }
@@ -637,6 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else if (warp >= 2) {
     // ---------------- epilogue (both CTAs, own 128 rows) ----------------
     const int quarter = warp & 3;
+    const int ehalf = (warp - 2) >> 2;         // which 32-token chunks of the tile this warp drains
     const int row = quarter * 32 + lane;
     const uint32_t leader_tempty0 = mapa_rank(lp::smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa_rank(lp::smem_u32(&tempty[1]), 0);
@@ -649,7 +655,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const int n = n0 + row;
       constexpr int CH = BT < 32 ? BT : 32;
-      for (int c = 0; c < BT; c += CH) {
+      for (int c = ehalf * CH; c < BT; c += 2 * CH) {
         uint32_t v[32], u[32];
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + a * C::ACC_COLS + c;
         if (CH == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
@@ -663,11 +669,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // instead of 64 B per token) — the SwiGLU tile is single-buffered,
           // so its epilogue is on the critical path
           __nv_bfloat16* xt = reinterpret_cast<__nv_bfloat16*>(smem + C::STAGES * C::STAGE_BYTES) +
-                              (size_t)quarter * 32 * C::XPOSE_PITCH;
+                              (size_t)(warp - 2) * 32 * C::XPOSE_PITCH;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float x = __uint_as_float(v[j]), up = __uint_as_float(u[j]);
-            xt[j * C::XPOSE_PITCH + lane] = __float2bfloat16_rn(x / (1.0f + __expf(-x)) * up);
+            xt[j * C::XPOSE_PITCH + lane] = __float2bfloat16_rn(__fdividef(x, 1.0f + __expf(-x)) * up);
           }
           __syncwarp();
           const int t = t0 + c + lane;
@@ -806,7 +812,7 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
       if (!sms2) LP_CUDA(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev));
       const int total = ((a.tiles_n + 1) / 2) * a.tiles_t * a.splits;
       const int clusters = total < sms2 / 2 ? total : sms2 / 2;
-      LP_CUDA(lp::launch(gemm_pair_kernel<BT, EPI>, dim3(2 * clusters), dim3(THREADS), Cfg2<BT, EPI>::SMEM, s, mw,
+      LP_CUDA(lp::launch(gemm_pair_kernel<BT, EPI>, dim3(2 * clusters), dim3(PAIR_THREADS), Cfg2<BT, EPI>::SMEM, s, mw,
                          mw2, mxh, a));
       return 0;
     }
