@@ -302,6 +302,17 @@ def run_reference(args):
 POISON = True
 
 
+def quiesce(distributed: bool) -> None:
+    """Host-side fence across ranks: every rank's previous scale-out (whose
+    relays may still be reading this rank's image) has finished."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if distributed:
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
 def timed_steps(so, steps, warmup, distributed, stream, want=None):
     """Device time per step (max over ranks).  With ``want`` (the source's
     per-block checksums) every step's verify-as-it-lands sums are checked;
@@ -312,6 +323,7 @@ def timed_steps(so, steps, warmup, distributed, stream, want=None):
     times, ok, launches = [], True, 0
     for i in range(warmup + steps):
         if POISON:
+            quiesce(distributed)         # every rank is done with the previous step (relays read peers)
             so.poison(0x5A ^ i, stream)  # receivers start every step without the model (untimed)
         if distributed:
             dist.barrier()
@@ -434,6 +446,7 @@ def main():
         my_nodes = so.cluster.exec_nodes
         e2e_times = []
         for i in range(args.warmup + args.steps):
+            quiesce(distributed)
             so.poison(0xC3 ^ i, stream)
             if distributed:
                 dist.barrier()
