@@ -97,7 +97,11 @@ int lp_mc_set_schedule(lp_mc* mc, const int32_t* xfers, int n_xfers,
                        const int32_t* sources, int n_sources);
 /* run every transfer whose executor is in exec_nodes (see lp_mc_configure);
  * push CTAs execute pushes, pull CTAs execute pulls; each exec node's kernel
- * also waits until every tile pushed into it this epoch landed. */
+ * also waits until every tile pushed into it this epoch landed.  Block
+ * counters of in-kernel pulls are re-based to (epoch - 1) x tiles first, so
+ * any later epoch works; runs with push CTAs need consecutive epochs.  After
+ * a watchdog failure (lp_mc_status -3) the handle refuses runs until
+ * lp_mc_reset_signals (then restart at epoch 1). */
 int lp_mc_run(lp_mc* mc, const int32_t* exec_nodes, int n_exec, uint32_t epoch,
               int push_ctas, int pull_ctas, void* stream);
 /* direction 0 = push: a GPU sender's CTAs store its blocks into the receiver
@@ -138,11 +142,14 @@ int lp_mc_run_host_dma(lp_mc* mc, int node, uint32_t epoch, int n_streams, void*
  * and record block_events[block] (created on that device).  Lets a caller
  * time per-block arrivals whichever executor/direction delivers them. */
 int lp_mc_landing_events(lp_mc* mc, int node, uint32_t epoch, void* stream, void* const* block_events);
-/* Verify-as-it-lands: zero sums_dev[n_blocks] (device memory) and launch
- * `ctas` CTAs on `stream` that checksum every block `node` receives this
- * epoch, tile by tile as its flags publish (either executor), with the
- * lp_block_checksums function; entries of blocks the node does not receive
- * stay 0.  Run it on a stream other than the multicast's. */
+/* Verify-as-it-lands: zero sums_dev[n_blocks] (device memory), then for every
+ * block `node` receives this epoch, in step order, enqueue on `stream` a
+ * stream-ordered wait on the node's own block counter (cuStreamWaitValue32,
+ * no SM held) followed by one checksum launch (<= `ctas` CTAs) over that
+ * block (the lp_block_checksums function); entries of blocks the node does
+ * not receive stay 0.  Enqueue it AFTER the epoch's producers (lp_mc_run /
+ * _run_ce / _run_host_dma), on another stream of the node's device: nothing
+ * then depends on cross-stream concurrency (runs under ncu's serialisation). */
 int lp_mc_verify(lp_mc* mc, int node, uint32_t epoch, int ctas, uint64_t* sums_dev, void* stream);
 /* number of ops node executes in-kernel (push + pull roles) and on the host
  * DMA path (0 unless host_dma) under the current configuration */
@@ -183,14 +190,18 @@ int lp_rmsnorm(const float* x, const void* w, int64_t T, int64_t d, float eps, v
 int lp_rmsnorm_zero(const float* x, const void* w, int64_t T, int64_t d, float eps, void* y, float* zero,
                     int64_t zero_cols, void* stream);
 /* RoPE (HF rotate_half) on q/k of qkv fp32 [T,(H+2KV)*hd]; q -> q_out bf16,
- * k/v appended to cache[seq][kv][pos][hd] bf16 */
+ * k appended to k_cache[seq][kv][pos][hd] bf16, v to v_cache (same layout)
+ * fp16 (attention's P.V runs in fp16) */
 int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim, const int32_t* pos,
                const int32_t* seq, float theta, void* q_out, void* k_cache, void* v_cache, int64_t max_len,
                void* stream);
-/* ragged causal GQA attention: token t attends to 0..pos[t] of seq[t].
- * head_dim 32..128 (multiple of 32), H/KV <= 8.  T*KV >= 1024 (prefill):
- * tensor-core tiles of 16 rows (mma.sync) when head_dim is 64 or 128 and the
- * tile's rows share a sequence; otherwise CUDA-core online softmax. */
+/* ragged causal GQA attention: token t attends to 0..pos[t] of seq[t]; k
+ * cache bf16, v cache fp16 (lp_rope_kv), out bf16.  head_dim 32..128
+ * (multiple of 32), H/KV <= 8.  T*KV >= 1024 (prefill), head_dim 64/128:
+ * tcgen05/TMEM kernel (128-row tiles of R tokens x H/KV heads, TMA-fed,
+ * fp32 S and O in TMEM; LP_ATTN_TC=0 selects the mma.sync kernel); decode:
+ * mma.sync kernels (few rows, K/V streaming bound; long caches split keys
+ * over a thread-block cluster); other head sizes: CUDA-core online softmax. */
 int lp_attention(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
                  const int32_t* seq, int64_t T, int n_heads, int n_kv, int head_dim, int64_t max_len,
                  float scale, void* out, void* stream);

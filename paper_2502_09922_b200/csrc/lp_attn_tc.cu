@@ -9,20 +9,22 @@
 //
 // Per 128-key chunk j of the tile's sequence:
 //   S_j  = Q K_j^T      tcgen05.mma kind::f16, A = Q (smem, K-major, bf16),
-//                       B = K_j (smem, K-major, bf16), D = S in TMEM (fp32)
-//   P_j  = exp2(S_j * scale * log2e - m_j)   softmax warps: TMEM -> regs,
+//                       B = K_j (smem, K-major, bf16), D = S in TMEM (fp32,
+//                       three buffers)
+//   P_j  = exp2(S_j * scale * log2e - m)     softmax warps: TMEM -> regs,
 //                       causal mask from pos[], fp16 P written to smem
-//   O_j  = P_j V_j      tcgen05.mma kind::f16, A = P (smem, K-major, fp16),
+//   O   += P_j V_j      tcgen05.mma kind::f16, A = P (smem, K-major, fp16),
 //                       B = V_j (smem, MN-major: the fp16 V cache is [key][hd]),
-//                       D = O_j in TMEM (fp32, a fresh buffer per chunk)
-//   O   <- O * 2^(m_{j-1} - m_j) + O_j       softmax warps, in registers
-// S and O are double-buffered in TMEM (2 x 128 + 2 x hd columns), K/V in two
-// smem stages and P in two smem buffers, so the MMAs of chunk j + 1 run
-// while the softmax warps work on chunk j.
+//                       D = O, accumulated in TMEM across all chunks
+// The row max m used for P only moves when the running max exceeds it by
+// more than 2^8 (P then stays <= 256, exact enough in fp16; the row sum l
+// uses the same m), so O almost never needs rescaling: when it does, the
+// row's softmax threads rescale it in TMEM (after the previous P V) before
+// releasing P_j.  Final: O / l.
 //
-//   warp 0   : TMA producer (Q once, then K/V chunks)
+//   warp 0   : TMA producer (Q once, then K chunks)      warp 10: TMA (V chunks)
 //   warp 1   : TMEM allocator + MMA issuer (one thread)
-//   warps 2-9: softmax / output (two threads per row: key / dim halves)
+//   warps 2-9: softmax (two threads per row: key / dim halves)
 //
 // A tile whose tokens belong to several sequences (ragged batches) walks the
 // chunks of each sequence run in turn with the other rows masked.
@@ -47,8 +49,8 @@ struct TcCfg {
   static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;    // 2 stages
   static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;    // 2 buffers
   static constexpr int SMEM = OFF_P + 2 * P_BYTES + 1024;
-  static constexpr int S_COL = 0;                       // S buffers: [0, 128), [128, 256)
-  static constexpr int O_COL = 2 * TC_KEYS;             // O buffers: [256, 256 + HD), [256 + HD, 256 + 2 HD)
+  static constexpr int S_COL = 0;                       // S buffers: [0, 128), [128, 256), [256, 384)
+  static constexpr int O_COL = 3 * TC_KEYS;             // O accumulator: [384, 384 + HD)
 };
 
 struct TcArgs {
@@ -99,6 +101,17 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+      "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+      "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -112,8 +125,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   using C = TcCfg<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_empty[2], p_full[2], o_full[2],
-      o_empty[2];
+  __shared__ __align__(8) uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[3], s_empty[3],
+      p_full[2], o_done;
   __shared__ uint32_t tmem_base;
   __shared__ int s_pos[TC_M];                 // per token of the tile (-1 past T)
   __shared__ int16_t s_seq[TC_M];
@@ -130,12 +143,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       lp::mbar_init(&k_empty[b], 1);
       lp::mbar_init(&v_full[b], 1);
       lp::mbar_init(&v_empty[b], 1);
+      lp::mbar_init(&p_full[b], 8);
+    }
+    for (int b = 0; b < 3; ++b) {
       lp::mbar_init(&s_full[b], 1);
       lp::mbar_init(&s_empty[b], 8);
-      lp::mbar_init(&p_full[b], 8);
-      lp::mbar_init(&o_full[b], 1);
-      lp::mbar_init(&o_empty[b], 8);
     }
+    lp::mbar_init(&o_done, 1);
     lp::fence_mbar_init();
   }
   if (warp == 1) {
@@ -213,89 +227,67 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       auto issue_pv = [&](int j) {
         const int b = j & 1;
-        lp::mbar_wait(&p_full[b], (j >> 1) & 1);
+        lp::mbar_wait(&p_full[b], (j >> 1) & 1);     // P_j written (and O rescaled if its rows needed it)
         lp::mbar_wait(&v_full[b], (j >> 1) & 1);
-        if (j >= 2) lp::mbar_wait(&o_empty[b], ((j >> 1) - 1) & 1);
         fence_after();
         const uint32_t sp = lp::smem_u32(sm + C::OFF_P + b * C::P_BYTES);
         const uint32_t sv = lp::smem_u32(sm + C::OFF_V + b * C::KV_BYTES);
 #pragma unroll
         for (int kk = 0; kk < TC_KEYS / 16; ++kk)
-          umma(tmem + C::O_COL + b * HD, desc_sw128(sp + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
-               desc_sw128(sv + kk * 2048, TC_KEYS * 128, 1024), idesc_pv, kk > 0);
-        commit(&o_full[b]);
+          umma(tmem + C::O_COL, desc_sw128(sp + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
+               desc_sw128(sv + kk * 2048, TC_KEYS * 128, 1024), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        commit(&o_done);
         commit(&v_empty[b]);
       };
       lp::mbar_wait(&q_full, 0);
       for (int it = 0; it < total; ++it) {
-        const int st = it & 1;
+        const int st = it & 1, sb = it % 3;
         lp::mbar_wait(&k_full[st], (it >> 1) & 1);
-        if (it >= 2) lp::mbar_wait(&s_empty[st], ((it >> 1) - 1) & 1);
+        if (it >= 3) lp::mbar_wait(&s_empty[sb], (it / 3 - 1) & 1);
         fence_after();
         const uint32_t sk = lp::smem_u32(sm + C::OFF_K + st * C::KV_BYTES);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          umma(tmem + C::S_COL + st * TC_KEYS, desc_sw128(sq + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
+          umma(tmem + C::S_COL + sb * TC_KEYS, desc_sw128(sq + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
                desc_sw128(sk + (kk >> 2) * (TC_KEYS * 128) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
-        commit(&s_full[st]);
+        commit(&s_full[sb]);
         commit(&k_empty[st]);
         if (it > 0) issue_pv(it - 1);
       }
       if (total > 0) issue_pv(total - 1);
     }
   } else if (warp <= 9) {
-    // ---------------- softmax / output ----------------
+    // ---------------- softmax ----------------
     // two warps per TMEM lane quarter: thread (row r, half h) owns keys
-    // [64h, 64h + 64) of every S chunk (= P atom h) and output dims
+    // [64h, 64h + 64) of every S chunk (= P atom h) and O columns
     // [h HD/2, (h + 1) HD/2); the row max is exchanged through smem once per
     // chunk (named barrier over the 256 softmax threads), the row sums only
-    // at the end (both halves scale by the same max).
+    // at the end (both halves use the same m).
     constexpr int HH = HD / 2;
+    constexpr float RESCALE = 8.0f;              // log2 headroom before m moves (P <= 2^8 in fp16)
     const int quarter = warp & 3;
     const int h = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const int i = r / a.G, g = r % a.G;
     const int prow = i < nvalid ? s_pos[i] : -1;
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    float o[HH];
-#pragma unroll
-    for (int d = 0; d < HH; ++d) o[d] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f, m_acc = -INFINITY;
-    float m_h0 = -INFINITY, m_h1 = -INFINITY;    // max used for P of the last even / odd chunk
-    auto merge = [&](int j) {
-      const int b = j & 1;
-      lp::mbar_wait(&o_full[b], (j >> 1) & 1);
-      fence_after();
-      const float mj = b ? m_h1 : m_h0;
-      const float sc = m_acc == -INFINITY ? 0.f : exp2f(m_acc - mj);
-      uint32_t v[HH];
-#pragma unroll
-      for (int cg = 0; cg < HH / 32; ++cg)
-        ld32(trow + C::O_COL + b * HD + h * HH + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cg * 32));
-      wait_ld();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[b]);
-#pragma unroll
-      for (int e = 0; e < HH; ++e) o[e] = fmaf(o[e], sc, __uint_as_float(v[e]));
-      m_acc = mj;
-    };
+    float m_use = -INFINITY, l_run = 0.f;
     int it = 0;
     for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
       run(lo, hi, sq, nch);
       const bool mine = i >= lo && i < hi;
       for (int c = 0; c < nch; ++c, ++it) {
-        const int b = it & 1;
-        lp::mbar_wait(&s_full[b], (it >> 1) & 1);
+        const int b = it & 1, sb = it % 3;
+        lp::mbar_wait(&s_full[sb], (it / 3) & 1);
         fence_after();
         const int lim = mine ? prow - c * TC_KEYS - h * 64 : -1;   // my keys 0..lim are visible
         uint32_t v[64];
-        ld32(trow + C::S_COL + b * TC_KEYS + h * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-        ld32(trow + C::S_COL + b * TC_KEYS + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        ld32(trow + C::S_COL + sb * TC_KEYS + h * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+        ld32(trow + C::S_COL + sb * TC_KEYS + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         wait_ld();
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[b]);   // S buffer b may be overwritten (S_{it+2})
+        if (lane == 0) mbar_arrive(&s_empty[sb]);  // S buffer may be overwritten (S_{it+3})
         // raw scores; the scale (> 0) is applied to the max and inside the exp FFMA
         float cmax = -INFINITY;
         if (lim >= 63) {                             // whole half below the diagonal: no mask
@@ -310,14 +302,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");   // previous chunk's partner max has been read
         s_mx[h][r] = cmax;
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        const float m_new = fmaxf(m_run, fmaxf(cmax, s_mx[h ^ 1][r]));
+        const float m_row = fmaxf(cmax, s_mx[h ^ 1][r]);
+        // both halves take the same decision from the same inputs; a row whose
+        // m was -inf has P = 0 so far, i.e. O = 0: nothing to rescale
+        const bool move = m_row > m_use + RESCALE || (m_use == -INFINITY && m_row > -INFINITY);
+        const float sc = (move && m_use != -INFINITY) ? exp2f(m_use - m_row) : 1.f;
+        const bool resc = move && m_use != -INFINITY && it > 0;
+        if (move) {
+          l_run *= m_use == -INFINITY ? 0.f : sc;
+          m_use = m_row;
+        }
+        if (__any_sync(0xffffffffu, resc)) {           // tcgen05.ld/st are warp-collective
+          lp::mbar_wait(&o_done, (it - 1) & 1);        // P_{it-1} V_{it-1} has landed
+          fence_after();
+          uint32_t o[HH];
+#pragma unroll
+          for (int cg = 0; cg < HH / 32; ++cg)
+            ld32(trow + C::O_COL + h * HH + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(o + cg * 32));
+          wait_ld();
+#pragma unroll
+          for (int e = 0; e < HH; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * sc);
+#pragma unroll
+          for (int cg = 0; cg < HH / 32; ++cg)
+            st32(trow + C::O_COL + h * HH + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(o + cg * 32));
+          wait_st();
+        }
         float lsum = 0.f;
         uint8_t* prow_s = sm + C::OFF_P + b * C::P_BYTES + h * ATOM + (r >> 3) * 1024 + (r & 7) * 128;
         if (lim < 0) {                               // nothing visible: P = 0
 #pragma unroll
           for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(prow_s + q * 16) = make_uint4(0, 0, 0, 0);
         } else {
-          const float nm = -m_new;
+          const float nm = -m_use;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {               // 8 x 16 B: keys 8q .. 8q + 7 of my 64
             uint32_t pk[4];
@@ -337,21 +353,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             *reinterpret_cast<uint4*>(prow_s + ((q ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
+        l_run += lsum;
+        fence_before();                              // TMEM stores (rescale) before the MMA reads O
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P stores -> visible to the MMA
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[b]);
-        const float al = m_run == -INFINITY ? 0.f : exp2f(m_run - m_new);
-        l_run = fmaf(l_run, al, lsum);
-        m_run = m_new;
-        if (b) m_h1 = m_new; else m_h0 = m_new;
-        if (it > 0) merge(it - 1);
       }
     }
-    if (it > 0) merge(it - 1);
     asm volatile("bar.sync 1, 256;" ::: "memory");
     s_mx[h][r] = l_run;
     asm volatile("bar.sync 1, 256;" ::: "memory");
     const float l_tot = l_run + s_mx[h ^ 1][r];
+    if (it > 0) {
+      lp::mbar_wait(&o_done, (it - 1) & 1);          // the last P V has landed
+      fence_after();
+    }
+    uint32_t o[HH];
+#pragma unroll
+    for (int cg = 0; cg < HH / 32; ++cg)
+      ld32(trow + C::O_COL + h * HH + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(o + cg * 32));
+    wait_ld();
     if (i < a.R && t0 + i < a.T && l_tot > 0.f) {
       const float inv = 1.0f / l_tot;
       __nv_bfloat16* orow = a.out + ((int64_t)(t0 + i) * a.H + kh * a.G + g) * HD + h * HH;
@@ -359,7 +380,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int d = 0; d < HH; d += 8) {
         __nv_bfloat162 w[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) w[e] = __floats2bfloat162_rn(o[d + 2 * e] * inv, o[d + 2 * e + 1] * inv);
+        for (int e = 0; e < 4; ++e)
+          w[e] = __floats2bfloat162_rn(__uint_as_float(o[d + 2 * e]) * inv, __uint_as_float(o[d + 2 * e + 1]) * inv);
         *reinterpret_cast<uint4*>(orow + d) = *reinterpret_cast<const uint4*>(w);
       }
     }
