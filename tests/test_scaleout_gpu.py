@@ -85,3 +85,32 @@ def test_sharded_host_load_verifies(n, executor, want):
                 assert r.checksums[node] == ref
     finally:
         so.close()
+
+
+@pytest.mark.parametrize("strategy", ["binary_tree", "broadcast_groups"])
+@pytest.mark.parametrize("executor", ["kernel", "ce"])
+def test_comparator_strategies_byte_exact(strategy, executor, want):
+    """The reference's comparator schedules (simengine.py:106-151, golden in
+    tests/test_hostpath_golden.py) executed by the same engine as λPipe —
+    only the schedule differs — deliver the source's bytes to every node
+    (5 emulated nodes on cuda:0, verify-as-it-lands sums == oracle)."""
+    import dataclasses
+    from paper_2502_09922_b200.cluster import b200_box, baseline_schedule
+    plan = SO.plan_scale_out("tiny", 5, k=1, block_count=4)
+    sched = baseline_schedule(strategy, plan.nodes, plan.layout.plan, b200_box(node_count=5))
+    plan = dataclasses.replace(plan, schedule=sched, strategy=strategy, pipelines=[])
+    so = SO.ScaleOut(plan, executor=executor, tile_bytes=1 << 20, pull_ctas=8, push_ctas=0,
+                     direction=1, copy_mode=0, verify=True, verify_ctas=8)
+    try:
+        so.load_sources()
+        ref = want(plan)
+        for _ in range(2):
+            for node in plan.receivers:
+                E.N.call("lp_memset", E.C.c_void_p(so.cluster.node(node).image), 0,
+                         plan.layout.weights_bytes, None)
+            r = so.run()
+            assert sorted(r.checksums) == plan.receivers
+            for node in plan.receivers:
+                assert r.checksums[node] == ref, (strategy, executor, node)
+    finally:
+        so.close()
