@@ -30,6 +30,8 @@
 // chunks of each sequence run in turn with the other rows masked.
 #include "lp_common.cuh"
 #include <cuda.h>
+#include <stdlib.h>
+#include <string.h>
 
 namespace {
 
@@ -59,7 +61,14 @@ struct TcArgs {
   __nv_bfloat16* out;
   int T, H, KV, G, R;
   float sl2;   // softmax scale * log2(e)
+  long long* trace;   // debug (LP_ATTN_TRACE): per-chunk clock64 stamps of the last CTA, else null
 };
+// trace slots per chunk: 0 S issued, 1 PV issued, 2 softmax S ready, 3 S loaded, 4 P written, 5 p_full arrive
+#define TRACE(slot, it)                                                                    \
+  do {                                                                                     \
+    if (a.trace && blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && (it) < 64)            \
+      a.trace[(it) * 8 + (slot)] = clock64();                                              \
+  } while (0)
 
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -114,6 +123,13 @@ __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&v)[32]) {
 __device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// 2^x on the SFU without exp2f's denormal-range fix-ups (P underflowing to 0
+// instead of a denormal is harmless): one MUFU.EX2
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lp::smem_u32(bar)) : "memory");
 }
@@ -230,6 +246,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         lp::mbar_wait(&p_full[b], (j >> 1) & 1);     // P_j written (and O rescaled if its rows needed it)
         lp::mbar_wait(&v_full[b], (j >> 1) & 1);
         fence_after();
+        TRACE(1, j);
         const uint32_t sp = lp::smem_u32(sm + C::OFF_P + b * C::P_BYTES);
         const uint32_t sv = lp::smem_u32(sm + C::OFF_V + b * C::KV_BYTES);
 #pragma unroll
@@ -251,6 +268,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           umma(tmem + C::S_COL + sb * TC_KEYS, desc_sw128(sq + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
                desc_sw128(sk + (kk >> 2) * (TC_KEYS * 128) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
         commit(&s_full[sb]);
+        TRACE(0, it);
         commit(&k_empty[st]);
         if (it > 0) issue_pv(it - 1);
       }
@@ -280,29 +298,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int b = it & 1, sb = it % 3;
         lp::mbar_wait(&s_full[sb], (it / 3) & 1);
         fence_after();
+        if (warp == 2 && lane == 0) TRACE(2, it);
         const int lim = mine ? prow - c * TC_KEYS - h * 64 : -1;   // my keys 0..lim are visible
+        const int limp = mine ? prow - c * TC_KEYS - (h ^ 1) * 64 : -1;   // the partner half's
+        // the row max over all 128 keys: own half kept in registers, the
+        // partner half streamed through 32 registers (TMEM reads are cheap;
+        // exchanging halves through smem cost two 256-thread barriers a chunk)
         uint32_t v[64];
+        float mx8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
+#pragma unroll
+        for (int cg = 0; cg < 2; ++cg) {
+          uint32_t w[32];
+          ld32(trow + C::S_COL + sb * TC_KEYS + (h ^ 1) * 64 + cg * 32, w);
+          wait_ld();
+          if (limp >= 63) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(w[e]));
+          } else if (limp >= 0) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (cg * 32 + e <= limp) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(w[e]));
+          }
+        }
         ld32(trow + C::S_COL + sb * TC_KEYS + h * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
         ld32(trow + C::S_COL + sb * TC_KEYS + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         wait_ld();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);  // S buffer may be overwritten (S_{it+3})
+        if (warp == 2 && lane == 0) TRACE(3, it);
         // raw scores; the scale (> 0) is applied to the max and inside the exp FFMA
-        float cmax = -INFINITY;
         if (lim >= 63) {                             // whole half below the diagonal: no mask
 #pragma unroll
-          for (int e = 0; e < 64; ++e) cmax = fmaxf(cmax, __uint_as_float(v[e]));
+          for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
         } else if (lim >= 0) {
 #pragma unroll
           for (int e = 0; e < 64; ++e)
-            if (e <= lim) cmax = fmaxf(cmax, __uint_as_float(v[e]));
+            if (e <= lim) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
         }
-        cmax *= a.sl2;
-        asm volatile("bar.sync 1, 256;" ::: "memory");   // previous chunk's partner max has been read
-        s_mx[h][r] = cmax;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const float m_row = fmaxf(cmax, s_mx[h ^ 1][r]);
+        const float m_row = a.sl2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         // both halves take the same decision from the same inputs; a row whose
         // m was -inf has P = 0 so far, i.e. O = 0: nothing to rescale
         const bool move = m_row > m_use + RESCALE || (m_use == -INFINITY && m_row > -INFINITY);
@@ -327,7 +364,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             st32(trow + C::O_COL + h * HH + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(o + cg * 32));
           wait_st();
         }
-        float lsum = 0.f;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};          // independent sum chains
         uint8_t* prow_s = sm + C::OFF_P + b * C::P_BYTES + h * ATOM + (r >> 3) * 1024 + (r & 7) * 128;
         if (lim < 0) {                               // nothing visible: P = 0
 #pragma unroll
@@ -340,24 +377,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
               const int k = q * 8 + e;
-              float p0 = exp2f(fmaf(__uint_as_float(v[k]), a.sl2, nm));
-              float p1 = exp2f(fmaf(__uint_as_float(v[k + 1]), a.sl2, nm));
+              float p0 = fast_exp2(fmaf(__uint_as_float(v[k]), a.sl2, nm));
+              float p1 = fast_exp2(fmaf(__uint_as_float(v[k + 1]), a.sl2, nm));
               if (lim < 63) {
                 p0 = k <= lim ? p0 : 0.f;
                 p1 = k + 1 <= lim ? p1 : 0.f;
               }
-              lsum += p0 + p1;
+              ls[e >> 1] += p0 + p1;
               const __half2 hv = __floats2half2_rn(p0, p1);
               pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
             }
             *reinterpret_cast<uint4*>(prow_s + ((q ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
-        l_run += lsum;
+        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         fence_before();                              // TMEM stores (rescale) before the MMA reads O
+        if (warp == 2 && lane == 0) TRACE(4, it);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P stores -> visible to the MMA
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[b]);
+        if (warp == 2 && lane == 0) TRACE(5, it);
       }
     }
     asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -441,9 +480,24 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     LP_CUDA(cudaFuncSetAttribute(attention_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr |= 1ull << dev;
   }
-  TcArgs args{pos, seq, (__nv_bfloat16*)out, T, H, KV, G, R, scale * 1.4426950408889634f};
+  static long long* trace = [] {
+    long long* t = nullptr;
+    if (getenv("LP_ATTN_TRACE")) cudaMallocManaged(&t, 64 * 8 * sizeof(long long));
+    return t;
+  }();
+  TcArgs args{pos, seq, (__nv_bfloat16*)out, T, H, KV, G, R, scale * 1.4426950408889634f, trace};
   const dim3 grid((unsigned)((T + R - 1) / R), (unsigned)KV);
   LP_CUDA(lp::launch(attention_tc_kernel<HD>, grid, dim3(TC_THREADS), C::SMEM, s, mq, mk, mv, args));
+  if (trace) {
+    LP_CUDA(cudaStreamSynchronize(s));
+    for (int it = 0; it < 64 && trace[it * 8]; ++it) {
+      const long long* t = trace + it * 8;
+      fprintf(stderr, "chunk %2d: S_issue %7lld PV_issue %7lld | sm: S_ready %7lld S_loaded %+6lld P_written %+6lld "
+              "arrive %+6lld\n", it, t[0] - trace[0], t[1] - trace[0], t[2] - trace[0], t[3] - t[2], t[4] - t[3],
+              t[5] - t[4]);
+    }
+    memset(trace, 0, 64 * 8 * sizeof(long long));
+  }
   return 0;
 }
 
