@@ -66,8 +66,8 @@ struct TcArgs {
 // trace slots per chunk: 0 S issued, 1 PV issued, 2 softmax S ready, 3 S loaded, 4 P written, 5 p_full arrive
 #define TRACE(slot, it)                                                                    \
   do {                                                                                     \
-    if (a.trace && blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && (it) < 64)            \
-      a.trace[(it) * 8 + (slot)] = clock64();                                              \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && (it) < 64)            \
+      a.trace[(it) * 16 + (slot)] = clock64();                                              \
   } while (0)
 
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int c = 0; c < nch; ++c, ++it) {
           const int st = it & 1;
           if (it >= 2) lp::mbar_wait(&empty[st], ((it >> 1) - 1) & 1);
+          TRACE(is_k ? 7 : 8, it);
           lp::mbar_expect_tx(&full[st], C::KV_BYTES);
           for (int at = 0; at < C::ATOMS; ++at)
             tma3d(base + st * C::KV_BYTES + at * (TC_KEYS * 128), map, &full[st], at * 64, c * TC_KEYS, row);
@@ -260,6 +261,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int it = 0; it < total; ++it) {
         const int st = it & 1, sb = it % 3;
         lp::mbar_wait(&k_full[st], (it >> 1) & 1);
+        TRACE(9, it);
         if (it >= 3) lp::mbar_wait(&s_empty[sb], (it / 3 - 1) & 1);
         fence_after();
         const uint32_t sk = lp::smem_u32(sm + C::OFF_K + st * C::KV_BYTES);
@@ -340,6 +342,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         const float m_row = a.sl2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                           fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        if (warp == 2 && lane == 0) TRACE(6, it);
         // both halves take the same decision from the same inputs; a row whose
         // m was -inf has P = 0 so far, i.e. O = 0: nothing to rescale
         const bool move = m_row > m_use + RESCALE || (m_use == -INFINITY && m_row > -INFINITY);
@@ -480,23 +483,30 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     LP_CUDA(cudaFuncSetAttribute(attention_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr |= 1ull << dev;
   }
-  static long long* trace = [] {
+  static long long* trace = [] {     // device memory: a managed buffer's page faults distort the stamps
     long long* t = nullptr;
-    if (getenv("LP_ATTN_TRACE")) cudaMallocManaged(&t, 64 * 8 * sizeof(long long));
+    if (getenv("LP_ATTN_TRACE")) {
+      cudaMalloc(&t, 64 * 16 * sizeof(long long));
+      cudaMemset(t, 0, 64 * 16 * sizeof(long long));
+    }
     return t;
   }();
   TcArgs args{pos, seq, (__nv_bfloat16*)out, T, H, KV, G, R, scale * 1.4426950408889634f, trace};
   const dim3 grid((unsigned)((T + R - 1) / R), (unsigned)KV);
   LP_CUDA(lp::launch(attention_tc_kernel<HD>, grid, dim3(TC_THREADS), C::SMEM, s, mq, mk, mv, args));
   if (trace) {
+    static long long h[64 * 16];
     LP_CUDA(cudaStreamSynchronize(s));
-    for (int it = 0; it < 64 && trace[it * 8]; ++it) {
-      const long long* t = trace + it * 8;
-      fprintf(stderr, "chunk %2d: S_issue %7lld PV_issue %7lld | sm: S_ready %7lld S_loaded %+6lld P_written %+6lld "
-              "arrive %+6lld\n", it, t[0] - trace[0], t[1] - trace[0], t[2] - trace[0], t[3] - t[2], t[4] - t[3],
-              t[5] - t[4]);
+    LP_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
+    const long long* tr0 = h;
+    for (int it = 0; it < 64 && h[it * 16]; ++it) {
+      const long long* t = h + it * 16;
+      fprintf(stderr, "chunk %2d: S_issue %7lld PV_issue %7lld | sm: S_ready %7lld S_loaded %+6lld max %+6lld "
+              "P_written %+6lld arrive %+6lld | K_issue %7lld V_issue %7lld K_landed %7lld\n", it, t[0] - tr0[0],
+              t[1] - tr0[0], t[2] - tr0[0], t[3] - t[2], t[6] - t[3], t[4] - t[6], t[5] - t[4], t[7] - tr0[0],
+              t[8] - tr0[0], t[9] - tr0[0]);
     }
-    memset(trace, 0, 64 * 8 * sizeof(long long));
+    LP_CUDA(cudaMemset(trace, 0, sizeof(h)));
   }
   return 0;
 }
