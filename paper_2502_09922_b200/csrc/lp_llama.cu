@@ -1043,7 +1043,10 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
       const char* e = getenv("LP_ATTN_TC");
       return e ? atoi(e) : 1;
     }();
-    if (tc_env) {
+    // short caches (<= 2 key chunks per tile) stay on the mma.sync kernel: a
+    // one-chunk tile is latency-bound on tcgen05 (16 x 128-token prompts:
+    // 35 vs 29 us per 8B layer, profiles/r02/attn_prefill_*_perf.txt)
+    if (tc_env && max_len > 256) {
       const int r = lp::attention_tc(q, k_cache, v_cache, pos, seq, T, n_heads, n_kv, head_dim, max_len, scale,
                                      out, s);
       if (r <= 0) return r;

@@ -23,6 +23,9 @@ pytestmark = pytest.mark.gpu
 # rounding points amplify accumulation-order noise (a 1e-7 relative weight
 # perturbation moves the bf16 oracle's own logits by 0.02, tests/test_prompts_golden.py),
 # so the committed prompts' margins clear 0.1 at every position instead.
+import os as _os
+TESTS_DIR = _os.path.dirname(_os.path.abspath(__file__))
+ROOT_DIR = _os.path.dirname(TESTS_DIR)
 LOGIT_TOL = 0.06
 LOGIT_TOL_FP32 = 0.1
 
@@ -77,6 +80,21 @@ def test_attention_matches_fp32(hd, H, KV, ctx, run):
     tiles when max_len's K/V fit (the last two cases; mixed-sequence tiles
     read global memory), else a warp per row."""
     _check_attention(hd, H, KV, ctx, run, max(ctx) + 8)
+
+
+@pytest.mark.parametrize("dbuf", ["1", "0"])
+def test_attention_decode_single_cta_double_buffer(dbuf, monkeypatch):
+    """The single-CTA double-buffered decode variant (no key split: T x KV in
+    [75, 148], cache >= 1024 keys — the 8B B = 10 x 1100-key case) and, as an
+    A/B, the single-buffered kernel (LP_DEC_DBUF=0, read once per process, so
+    run in a subprocess)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r); import test_decoder_gpu as t; "
+            "t._check_attention(128, 32, 8, [1100] * 10, 0, 1200)") % (ROOT_DIR, TESTS_DIR)
+    env = dict(__import__("os").environ, LP_DEC_DBUF=dbuf)
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=240)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
 
 
 @pytest.mark.parametrize("hd,H,KV,ctx,max_len", [(128, 32, 8, [4000], 4096), (64, 4, 2, [1, 1500, 700], 1536),
@@ -215,16 +233,17 @@ def test_generate_api_matches_oracle(tiny):
     assert compared == 48
 
 
-@pytest.mark.parametrize("hd,H,KV,lens", [(128, 32, 8, [1024]), (128, 64, 8, [700, 300]), (128, 8, 8, [517]),
-                                           (64, 4, 2, [600, 1, 33]), (128, 32, 8, [64] * 9 + [130])])
-def test_prefill_attention_tcgen05_causal(hd, H, KV, lens):
+@pytest.mark.parametrize("hd,H,KV,lens,cap", [(128, 32, 8, [1024], 0), (128, 64, 8, [700, 300], 0),
+                                               (128, 8, 8, [517], 0), (64, 4, 2, [600, 1, 33], 0),
+                                               (128, 32, 8, [64] * 9 + [130], 400)])
+def test_prefill_attention_tcgen05_causal(hd, H, KV, lens, cap):
     """Prompts laid out as consecutive rows (the serving layout: one or more
     sequences back to back, positions 0..len-1) through the tcgen05/TMEM
     prefill kernel (lp_attn_tc.cu), vs a torch fp32 causal softmax over the
     same bf16 K / fp16 V caches."""
     import torch
     g = torch.Generator(device="cuda").manual_seed(sum(lens) + hd + H)
-    seqs, max_len = len(lens), max(lens) + 16
+    seqs, max_len = len(lens), max(max(lens) + 16, cap)     # caches > 256 keys take the tcgen05 kernel
     kc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.bfloat16)
     vc = torch.randn(seqs, KV, max_len, hd, device="cuda", generator=g).to(torch.float16)
     pos = [p for n in lens for p in range(n)]
