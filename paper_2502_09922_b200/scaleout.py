@@ -166,6 +166,11 @@ class TieredPlan:
     plan: ScaleOutPlan | None
     ref_nodes: list
     host_id: int | None
+    # what the engine executes: the λPipe plan plus, when warm nodes load
+    # from host memory, their k-way-ordered loads and warm pipeline
+    # (warm_pipeline_plan); exec_ref_nodes[i] = reference id of position i
+    exec_plan: ScaleOutPlan | None = None
+    exec_ref_nodes: list = field(default_factory=list)
 
     def position(self, ref_node: int) -> int:
         return self.ref_nodes.index(ref_node)
@@ -237,6 +242,71 @@ def plan_from_tiers(config, demand: list, tiers: TierMap, k: int = 1, block_coun
     hosts = tuple(i for i, n in enumerate(sources) if tier_of(n) == MEMORY)
     plan = plan_scale_out(cfg, len(ref_nodes), k_eff, block_count, cluster=cluster, host_nodes=hosts)
     return TieredPlan(sp, hot, warm, cold, sources, plan, ref_nodes, host_id)
+
+
+def warm_pipeline_plan(tp: TieredPlan, config, block_count: int, cluster: ClusterSpec | None = None) -> TieredPlan:
+    """Execution plan with warm-node pipelines (the
+    reference simulator specifies but does not implement them, loading warm
+    nodes in block order and serving only after the full load,
+    simengine.py:507-521).
+
+    The W warm demand nodes load from the host copy in k-way order — warm node
+    i first loads chunk i of ``k_way_orders(b, W)`` (multicast.py:246-265),
+    each over its own PCIe link — and form one execution pipeline among
+    themselves (stage i = chunk i), planned with the reference's own
+    ``completion_ordered_groups`` / ``generate_pipelines`` /
+    ``assign_blocks_to_stages`` over the warm loads as W one-receiver groups,
+    so it activates after about 1/W of the load.  The rows run on the same
+    engine as the λPipe multicast (same counters, same activation logic).
+    Sets ``tp.exec_plan`` / ``tp.exec_ref_nodes`` and returns ``tp``."""
+    cfg = CONFIGS[config] if isinstance(config, str) else config
+    base = tp.plan
+    if not tp.warm:
+        tp.exec_plan, tp.exec_ref_nodes = base, list(tp.ref_nodes)
+        return tp
+    layout = base.layout if base is not None else build_layout(cfg, block_count)
+    b = layout.plan.block_count
+    refs = list(tp.ref_nodes) if base is not None else []
+    steps = [list(row) for row in base.schedule.steps] if base is not None else []
+    groups = list(base.groups) if base is not None else []
+    sources = list(base.sources) if base is not None else []
+    hosts = list(base.host_nodes) if base is not None else []
+    pipes = list(base.pipelines) if base is not None else []
+    ordered = list(base.ordered) if base is not None else []
+    # warm node i reads its "own host memory" — a HOST position over the one
+    # pinned copy per warm node — so every load is a one-receiver sub-group
+    # and the λPipe groups stay disjoint
+    W = len(tp.warm)
+    orders = k_way_orders(b, W)
+    hpos = list(range(len(refs), len(refs) + W))
+    refs += [tp.host_id if tp.host_id is not None else -1] * W
+    sources += hpos
+    hosts += hpos
+    wpos = list(range(len(refs), len(refs) + W))
+    refs += list(tp.warm)
+    wsteps = [[Transfer(st, hpos[i], wpos[i], orders[i][st]) for i in range(W)] for st in range(b)]
+    # the warm pipeline, planned on its own (group ids 0..W-1, as the
+    # reference's pipeline functions index the k-way orders by group id)
+    local = [SubGroup(i, (hpos[i], wpos[i]), tuple(orders[i])) for i in range(W)]
+    wsched = MulticastSchedule(tuple(local), wsteps, max_send_degree=1, enforce_step_bound=False, label="warm")
+    wordered = completion_ordered_groups(local, wsched)
+    for pn in generate_pipelines(wordered):
+        ep = assign_blocks_to_stages(pn, [g.transfer_order for g in wordered], b, wsched, len(pipes))
+        pipes.append(ep)
+    wgroups = [SubGroup(len(groups) + i, g.member_nodes, g.transfer_order) for i, g in enumerate(local)]
+    for st, row in enumerate(wsteps):
+        while len(steps) <= st:
+            steps.append([])
+        steps[st] = steps[st] + row
+    deg = base.schedule.max_send_degree if base is not None else 1
+    sched = MulticastSchedule(tuple(groups + wgroups), steps, max_send_degree=deg, enforce_step_bound=False,
+                              label="lambda+warm")
+    step_s = base.step_s_model if base is not None else transfer_step_time(wsched, layout.plan,
+                                                                             cluster or b200_box(node_count=len(refs)))
+    tp.exec_plan = ScaleOutPlan(cfg, layout, list(range(len(refs))), sources, groups + wgroups, sched,
+                                ordered + wgroups, pipes, step_s, True, "lambda+warm", tuple(hosts))
+    tp.exec_ref_nodes = refs
+    return tp
 
 
 def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
@@ -444,70 +514,57 @@ class ScaleOut:
 
 class TieredScaleOut:
     """Executes a :class:`TieredPlan` on this process's GPUs (one process,
-    ``engine.Cluster.devices``): position i of the multicast lives on device
-    ``node_devices[ref_nodes[i]]`` (the HOST node in pinned host memory),
-    warm demand nodes load every block from the host copy over their own
-    PCIe link (copy engine, block order), hot ones keep their copy.  The
+    ``engine.Cluster.devices``) through its execution plan
+    (:func:`warm_pipeline_plan`): the λPipe multicast to the cold nodes plus
+    the warm nodes' k-way-ordered loads from the pinned host copy, all rows on
+    one engine (position i on device ``node_devices[exec_ref_nodes[i]]``,
+    HOST positions in pinned memory); hot nodes keep their copy.  The
     multicast runs in-kernel in the pull direction (receivers read peers over
-    NVLink and the host over PCIe)."""
+    NVLink and the host over PCIe).  ``plan`` is what ``serving.Server``
+    takes: its pipelines include the warm pipeline."""
 
     def __init__(self, tp: TieredPlan, node_devices: dict | None = None, seed: int = 0,
-                 tile_bytes: int = 1 << 20):
+                 tile_bytes: int = 1 << 20, config=None, block_count: int | None = None):
         self.tp = tp
         self.seed = seed
         self.dev_of = dict(node_devices or {})
         self.cluster = None
-        self.warm_images = {}
-        self.host = None
-        if tp.plan is not None:
-            lay = tp.plan.layout
-            devs = [-1 if i in tp.plan.host_nodes else self.dev_of.get(n, n) for i, n in enumerate(tp.ref_nodes)]
+        if tp.exec_plan is None:
+            cfg = config or (tp.plan.config if tp.plan is not None else None)
+            warm_pipeline_plan(tp, cfg, block_count or (tp.plan.block_count if tp.plan is not None else 16))
+        plan = tp.exec_plan
+        self.layout = plan.layout if plan is not None else None
+        if plan is not None:
+            lay = plan.layout
+            devs = [-1 if i in plan.host_nodes else self.dev_of.get(n, n) for i, n in enumerate(tp.exec_ref_nodes)]
             self.cluster = E.Cluster.devices(devs, lay.block_offsets, lay.block_lengths, lay.weights_bytes,
                                              tile_bytes=tile_bytes)
-            self.host = self.cluster.host
 
     @property
     def plan(self):
-        return self.tp.plan
-
-    def load_sources(self, layout=None):
-        lay = layout or self.tp.plan.layout
-        self.layout = lay
-        if self.cluster is not None:
-            for i in self.tp.plan.sources:
-                E.load_source_image(self.cluster, i, lay, self.seed, device=self._any_device())
-            self.cluster.set_schedule_all(self.tp.plan.schedule, self.tp.plan.sources)
-        if self.tp.warm:
-            if self.host is None:
-                with E.on_device(self._any_device()):
-                    self.host = E.HostImage(lay.weights_bytes)
-                scratch = E.dev_malloc(self._any_device(), lay.weights_bytes)
-                with E.on_device(self._any_device()):
-                    E.fill_image(scratch, lay, self.seed)
-                    E.N.call("lp_memcpy", E.C.c_void_p(self.host.host_ptr), E.C.c_void_p(scratch),
-                             lay.weights_bytes, None)
-                E.N.call("lp_sync_device", self._any_device())
-                E.dev_free(self._any_device(), scratch)
-            for w in self.tp.warm:
-                d = self.dev_of.get(w, w)
-                self.warm_images[w] = (d, E.dev_malloc(d, lay.weights_bytes))
+        return self.tp.exec_plan
 
     def _any_device(self) -> int:
-        return min([self.dev_of.get(n, n) for n in (self.tp.ref_nodes or self.tp.warm or self.tp.hot)
-                    if n != self.tp.host_id] or [0])
+        devs = [nb.device for nb in self.cluster.nodes if nb.device >= 0] if self.cluster else [0]
+        return min(devs)
+
+    def load_sources(self):
+        if self.cluster is None:
+            return
+        plan = self.tp.exec_plan
+        filled_host = False
+        for i in plan.sources:
+            nb = self.cluster.node(i)
+            if nb.kind == E.LP_NODE_HOST:
+                if filled_host:
+                    continue
+                filled_host = True
+            E.load_source_image(self.cluster, i, plan.layout, self.seed, device=self._any_device())
+        self.cluster.set_schedule_all(plan.schedule, plan.sources)
 
     def launch(self, streams: dict, pull_ctas: int = 32) -> int | None:
-        """Start the multicast (one kernel per device on ``streams[device]``)
-        and the warm nodes' host loads; returns the multicast epoch."""
-        import torch
-        lay = self.layout
-        for w, (d, img) in self.warm_images.items():
-            st = streams[d]
-            with torch.cuda.stream(st):
-                for b in range(len(lay.block_offsets)):      # block order (the reference's h2d chunks)
-                    o, n = lay.block_offsets[b], lay.block_lengths[b]
-                    E.N.call("lp_memcpy", E.C.c_void_p(img + o), E.C.c_void_p(self.host.host_ptr + o), n,
-                             E.C.c_void_p(st.cuda_stream))
+        """Start the multicast + warm loads (one kernel per device on
+        ``streams[device]``); returns the epoch."""
         if self.cluster is None:
             return None
         return self.cluster.launch_devices(streams, 0, pull_ctas)
@@ -520,30 +577,23 @@ class TieredScaleOut:
 
     def checksums(self) -> dict:
         """reference node id -> per-block checksums of every demand node's copy."""
-        lay = self.layout
         out = {}
-        if self.cluster is not None:
-            for i, n in enumerate(self.tp.ref_nodes):
-                if i in self.tp.plan.sources:
-                    continue
-                nb = self.cluster.node(i)
-                with E.on_device(nb.device):
-                    out[n] = E.block_checksums(nb.image, lay.block_offsets, lay.block_lengths)
-        for w, (d, img) in self.warm_images.items():
-            with E.on_device(d):
-                out[w] = E.block_checksums(img, lay.block_offsets, lay.block_lengths)
+        if self.cluster is None:
+            return out
+        plan = self.tp.exec_plan
+        lay = plan.layout
+        for i, n in enumerate(self.tp.exec_ref_nodes):
+            if i in plan.sources:
+                continue
+            nb = self.cluster.node(i)
+            with E.on_device(nb.device):
+                out[n] = E.block_checksums(nb.image, lay.block_offsets, lay.block_lengths)
         return out
 
     def close(self):
-        for w, (d, img) in self.warm_images.items():
-            E.dev_free(d, img)
-        self.warm_images = {}
         if self.cluster is not None:
             self.cluster.close()
             self.cluster = None
-        elif self.host is not None:
-            self.host.close()
-        self.host = None
 
 
 def scale_out(model, demand: list, tiers: TierMap, k: int = 1, block_count: int = 16, host_id: int | None = None,
@@ -551,15 +601,18 @@ def scale_out(model, demand: list, tiers: TierMap, k: int = 1, block_count: int 
     """Drop-in entry for the simulator's scale-out of
     ``demand`` nodes (simengine.py:442-467 then :564-602) on real GPUs:
     ``startup_plan`` over ``tiers`` (GPU copies first, then the box's host
-    copy ``host_id``), hot nodes kept, warm nodes loaded from host memory,
-    the λPipe multicast to the cold ones executed and waited for.  Returns
+    copy ``host_id``), hot nodes kept, warm nodes loaded from host memory in
+    k-way order (with their pipeline, :func:`warm_pipeline_plan`), the λPipe
+    multicast to the cold ones — executed and waited for.  Returns
     ``(TieredScaleOut, epoch)``; the caller closes it."""
     import torch
-    tp = plan_from_tiers(model, demand, tiers, k, block_count, host_id)
+    cfg = CONFIGS[model] if isinstance(model, str) else model
+    tp = warm_pipeline_plan(plan_from_tiers(cfg, demand, tiers, k, block_count, host_id), cfg, block_count)
     so = TieredScaleOut(tp, node_devices, seed)
-    so.load_sources(tp.plan.layout if tp.plan is not None else build_layout(
-        CONFIGS[model] if isinstance(model, str) else model, block_count))
-    devs = sorted({so.dev_of.get(n, n) for n in tp.ref_nodes + tp.warm if n != host_id})
+    so.load_sources()
+    if so.cluster is None:
+        return so, None
+    devs = sorted({nb.device for nb in so.cluster.nodes if nb.device >= 0})
     streams = {d: torch.cuda.Stream(device=d) for d in devs}
     epoch = so.launch(streams, pull_ctas)
     so.wait(streams)

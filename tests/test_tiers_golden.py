@@ -49,3 +49,27 @@ def test_box_tiers_host_copy_after_gpu_copies():
     tm = SO.box_tiers("tiny", 4, gpu_resident=(), host_copy=True, host_id=4)
     tp = SO.plan_from_tiers("tiny", [0, 1, 2, 3], tm, k=2, block_count=4, host_id=4)
     assert tp.sources == [4] and tp.plan.host_nodes == (0,)
+
+
+def test_warm_pipeline_plan_shapes():
+    """Warm-node pipelines: warm node i loads chunk i of
+    the k-way orders first; the warm pipeline's stage i holds chunk i and
+    activates once every stage's chunk has landed; the combined execution
+    schedule (λPipe rows + warm loads) passes the reference's validator."""
+    from paper_2502_09922_b200.multicast import k_way_orders, validate_schedule
+    tm = SO.box_tiers("tiny", 4, gpu_resident=(0,), host_copy=True, host_id=6, warm=(3, 4))
+    tp = SO.warm_pipeline_plan(SO.plan_from_tiers("tiny", [1, 2, 3, 4, 5], tm, k=2, block_count=4, host_id=6),
+                               "tiny", 4)
+    p = tp.exec_plan
+    assert tp.cold == [1, 2, 5] and tp.warm == [3, 4] and tp.sources == [0, 3]
+    assert validate_schedule(p.schedule) == []
+    warm_pos = [i for i, n in enumerate(tp.exec_ref_nodes) if n in tp.warm and i not in p.sources]
+    orders = k_way_orders(4, 2)
+    for w, order in zip(warm_pos, orders):
+        got = [t.block_id for row in p.schedule.steps for t in row if t.receiver == w]
+        assert got == list(order)
+    ep = p.pipelines[-1]
+    assert [st.node for st in ep.stages] == warm_pos
+    assert [(st.block_lo, st.block_hi) for st in ep.stages] == [(0, 1), (2, 3)] and ep.activation_step == 1
+    # the λPipe part is untouched
+    assert p.pipelines[:len(tp.plan.pipelines)] == tp.plan.pipelines
