@@ -436,6 +436,296 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ping-pong variant: TWO Q tiles per CTA (tokens [t0, t0 + R) and
+// [t0 + R, t0 + 2R) of one kv head) over 64-key chunks.  Each tile has its own
+// softmax warpgroup (warps 2-5: tile 0, warps 6-9: tile 1; one thread per row
+// holds the chunk's whole 64-key row, so no max exchange), its own two S
+// buffers and O accumulator in TMEM (2 x (2 x 64 + 128) = 512 columns), and
+// two P buffers; K/V chunks are shared.  While one tile's warps sit in TMEM
+// loads / max / P stores the other's use the SFU, and the MMAs of one tile run
+// under the other's softmax (FA4-style), which the one-tile kernel's lock-step
+// half-row warps could not do (its measured chunk: ~2,300 softmax cycles vs
+// ~1,100 MMA cycles, profiles/r02/attn_tc_chunk_trace_8b_1x2048.txt).
+constexpr int PP_KEYS = 64;
+constexpr int PP_THREADS = 352;
+
+template <int HD>
+struct PpCfg {
+  static constexpr int ATOMS = HD / 64;
+  static constexpr int Q_BYTES = TC_M * HD * 2;          // one tile
+  static constexpr int KV_BYTES = PP_KEYS * HD * 2;      // one chunk
+  static constexpr int P_BYTES = TC_M * PP_KEYS * 2;     // one tile's chunk = one 128B-swizzle atom
+  static constexpr int OFF_Q = 0;                        // 2 tiles
+  static constexpr int OFF_K = 2 * Q_BYTES;              // 2 stages
+  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;     // 2 stages
+  static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;     // [tile][2]
+  static constexpr int SMEM = OFF_P + 4 * P_BYTES + 1024;
+  static constexpr int TILE_COLS = 256;                  // per tile: S0 [0,64), S1 [64,128), O [128, 128 + HD)
+};
+
+template <int HD>
+__global__ void __launch_bounds__(PP_THREADS, 1)
+    attention_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const TcArgs a) {
+  using C = PpCfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2][2], s_empty[2][2],
+      p_full[2][2], o_done[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ int s_pos[2 * TC_M];
+  __shared__ int16_t s_seq[2 * TC_M];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = gridDim.x - 1 - blockIdx.x;          // later (longer) tiles first: causal balance
+  const int kh = blockIdx.y;
+  const int R2 = 2 * a.R;
+  const int t0 = tile * R2;
+
+  if (threadIdx.x == 0) {
+    lp::mbar_init(&q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      lp::mbar_init(&k_full[b], 1);
+      lp::mbar_init(&k_empty[b], 1);
+      lp::mbar_init(&v_full[b], 1);
+      lp::mbar_init(&v_empty[b], 1);
+      for (int t = 0; t < 2; ++t) {
+        lp::mbar_init(&s_full[t][b], 1);
+        lp::mbar_init(&s_empty[t][b], 4);
+        lp::mbar_init(&p_full[t][b], 4);
+      }
+      lp::mbar_init(&o_done[b], 1);
+    }
+    lp::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     lp::smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+  }
+  lp::pdl_wait();
+  lp::pdl_trigger();
+  for (int i = threadIdx.x; i < R2; i += blockDim.x) {
+    const bool v = t0 + i < a.T;
+    s_pos[i] = v ? a.pos[t0 + i] : -1;
+    s_seq[i] = v ? (int16_t)a.seq[t0 + i] : (int16_t)-1;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base;
+  auto run = [&](int lo, int& hi, int& sq, int& chunks) {
+    sq = s_seq[lo];
+    chunks = 0;
+    for (hi = lo; hi < R2 && s_seq[hi] == sq; ++hi) chunks = max(chunks, (s_pos[hi] + PP_KEYS) / PP_KEYS);
+  };
+  const int nvalid = min(R2, a.T - t0);
+
+  if (warp == 0 || warp == 10) {
+    if (lane == 0) {
+      const bool is_k = warp == 0;
+      if (is_k) {
+        lp::mbar_expect_tx(&q_full, 2 * C::Q_BYTES);
+        for (int t = 0; t < 2; ++t)
+          for (int at = 0; at < C::ATOMS; ++at)
+            tma3d(sm + C::OFF_Q + t * C::Q_BYTES + at * ATOM, &tmQ, &q_full, at * 64, kh * a.G, t0 + t * a.R);
+      }
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      const CUtensorMap* map = is_k ? &tmK : &tmV;
+      uint8_t* base = sm + (is_k ? C::OFF_K : C::OFF_V);
+      int it = 0;
+      for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+        run(lo, hi, sq, nch);
+        const int row = sq * a.KV + kh;
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int st = it & 1;
+          if (it >= 2) lp::mbar_wait(&empty[st], ((it >> 1) - 1) & 1);
+          lp::mbar_expect_tx(&full[st], C::KV_BYTES);
+          for (int at = 0; at < C::ATOMS; ++at)
+            tma3d(base + st * C::KV_BYTES + at * (PP_KEYS * 128), map, &full[st], at * 64, c * PP_KEYS, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(PP_KEYS >> 3) << 17) |
+                                   ((uint32_t)(TC_M >> 4) << 24);
+      constexpr uint32_t idesc_pv = (1u << 4) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) |
+                                    ((uint32_t)(TC_M >> 4) << 24);
+      int total = 0;
+      for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+        run(lo, hi, sq, nch);
+        total += nch;
+      }
+      auto issue_pv = [&](int j) {
+        const int b = j & 1;
+        lp::mbar_wait(&v_full[b], (j >> 1) & 1);
+        const uint32_t sv = lp::smem_u32(sm + C::OFF_V + b * C::KV_BYTES);
+        for (int t = 0; t < 2; ++t) {
+          lp::mbar_wait(&p_full[t][b], (j >> 1) & 1);
+          fence_after();
+          const uint32_t sp = lp::smem_u32(sm + C::OFF_P + (t * 2 + b) * C::P_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < PP_KEYS / 16; ++kk)
+            umma(tmem + t * C::TILE_COLS + 128, desc_sw128(sp + kk * 32, 16, 1024),
+                 desc_sw128(sv + kk * 2048, PP_KEYS * 128, 1024), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          commit(&o_done[t]);
+        }
+        commit(&v_empty[b]);
+      };
+      lp::mbar_wait(&q_full, 0);
+      for (int it = 0; it < total; ++it) {
+        const int st = it & 1;
+        lp::mbar_wait(&k_full[st], (it >> 1) & 1);
+        const uint32_t sk = lp::smem_u32(sm + C::OFF_K + st * C::KV_BYTES);
+        for (int t = 0; t < 2; ++t) {
+          if (it >= 2) lp::mbar_wait(&s_empty[t][st], ((it >> 1) - 1) & 1);
+          fence_after();
+          const uint32_t sq = lp::smem_u32(sm + C::OFF_Q + t * C::Q_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            umma(tmem + t * C::TILE_COLS + st * PP_KEYS,
+                 desc_sw128(sq + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
+                 desc_sw128(sk + (kk >> 2) * (PP_KEYS * 128) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
+          commit(&s_full[t][st]);
+        }
+        commit(&k_empty[st]);
+        if (it > 0) issue_pv(it - 1);
+      }
+      if (total > 0) issue_pv(total - 1);
+    }
+  } else if (warp <= 9) {
+    // ---------------- softmax: warpgroup t owns Q tile t, thread = row ----------------
+    constexpr float RESCALE = 8.0f;
+    const int t = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int i = t * a.R + r / a.G, g = r % a.G;    // token index within the CTA's 2R tokens
+    const int prow = i < nvalid ? s_pos[i] : -1;
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16) + t * C::TILE_COLS;
+    float m_use = -INFINITY, l_run = 0.f;
+    int it = 0;
+    for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+      run(lo, hi, sq, nch);
+      const bool mine = i >= lo && i < hi;
+      for (int c = 0; c < nch; ++c, ++it) {
+        const int b = it & 1;
+        lp::mbar_wait(&s_full[t][b], (it >> 1) & 1);
+        fence_after();
+        const int lim = mine ? prow - c * PP_KEYS : -1;     // keys 0..lim of this chunk are visible
+        uint32_t v[64];
+        ld32(trow + b * PP_KEYS, *reinterpret_cast<uint32_t(*)[32]>(v));
+        ld32(trow + b * PP_KEYS + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        wait_ld();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[t][b]);
+        float mx8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
+        if (lim >= 63) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
+        } else if (lim >= 0) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (e <= lim) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
+        }
+        const float m_row = a.sl2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const bool move = m_row > m_use + RESCALE || (m_use == -INFINITY && m_row > -INFINITY);
+        const float sc = (move && m_use != -INFINITY) ? exp2f(m_use - m_row) : 1.f;
+        const bool resc = move && m_use != -INFINITY && it > 0;
+        if (move) {
+          l_run *= m_use == -INFINITY ? 0.f : sc;
+          m_use = m_row;
+        }
+        if (__any_sync(0xffffffffu, resc)) {           // rescale O in TMEM (warp-collective ld/st)
+          lp::mbar_wait(&o_done[t], (it - 1) & 1);
+          fence_after();
+#pragma unroll
+          for (int cg = 0; cg < HD / 32; ++cg) {
+            uint32_t o[32];
+            ld32(trow + 128 + cg * 32, o);
+            wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * sc);
+            st32(trow + 128 + cg * 32, o);
+          }
+          wait_st();
+        }
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        uint8_t* prow_s = sm + C::OFF_P + (t * 2 + b) * C::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
+        if (lim < 0) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(prow_s + q * 16) = make_uint4(0, 0, 0, 0);
+        } else {
+          const float nm = -m_use;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const int k = q * 8 + e;
+              float p0 = fast_exp2(fmaf(__uint_as_float(v[k]), a.sl2, nm));
+              float p1 = fast_exp2(fmaf(__uint_as_float(v[k + 1]), a.sl2, nm));
+              if (lim < 63) {
+                p0 = k <= lim ? p0 : 0.f;
+                p1 = k + 1 <= lim ? p1 : 0.f;
+              }
+              ls[e >> 1] += p0 + p1;
+              const __half2 hv = __floats2half2_rn(p0, p1);
+              pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+            }
+            *reinterpret_cast<uint4*>(prow_s + ((q ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
+        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        fence_before();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t][b]);
+      }
+    }
+    if (it > 0) {
+      lp::mbar_wait(&o_done[t], (it - 1) & 1);
+      fence_after();
+    }
+    const bool live = i < nvalid && l_run > 0.f;
+    const float inv = live ? 1.0f / l_run : 0.f;
+    __nv_bfloat16* orow = a.out + ((int64_t)(t0 + i) * a.H + kh * a.G + g) * HD;
+#pragma unroll
+    for (int cg = 0; cg < HD / 32; ++cg) {
+      uint32_t o[32];
+      ld32(trow + 128 + cg * 32, o);
+      wait_ld();
+      if (live) {
+#pragma unroll
+        for (int d = 0; d < 32; d += 8) {
+          __nv_bfloat162 w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            w[e] = __floats2bfloat162_rn(__uint_as_float(o[d + 2 * e]) * inv, __uint_as_float(o[d + 2 * e + 1]) * inv);
+          *reinterpret_cast<uint4*>(orow + cg * 32 + d) = *reinterpret_cast<const uint4*>(w);
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 typedef CUresult (*PFN_encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -467,14 +757,25 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   using C = TcCfg<HD>;
   const int G = H / KV;
   const int R = TC_M / G;
+  // LP_ATTN_TC: 1 = one Q tile per CTA (default), 2 = the ping-pong variant.
+  // Measured (profiles/r02/attn_prefill_pingpong_ab.txt): ping-pong wins on
+  // many short prompts (8 x 512 rows: 84 -> 70 us 8B, 143 -> 109 us 70B) and
+  // loses on one long one (1 x 2048: 83 -> 94 us, half as many, twice as long
+  // CTAs on 148 SMs); its two softmax warpgroups stay in phase, so the SFU /
+  // MMA overlap it was built for does not materialise yet.
+  static const int variant = [] {
+    const char* e = getenv("LP_ATTN_TC");
+    return e ? atoi(e) : 1;
+  }();
+  const uint32_t kbox = variant == 2 ? PP_KEYS : TC_KEYS;
   CUtensorMap mq, mk, mv;
   const uint64_t rows = (uint64_t)1 << 24;   // sequence x kv-head rows of the caches (unbounded here)
   if (map3d(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, q, HD, H, T, (uint64_t)HD * 2, (uint64_t)H * HD * 2, G, R)) return -1;
   if (map3d(&mk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, k_cache, HD, max_len, rows, (uint64_t)HD * 2,
-            (uint64_t)max_len * HD * 2, TC_KEYS, 1))
+            (uint64_t)max_len * HD * 2, kbox, 1))
     return -1;
   if (map3d(&mv, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, v_cache, HD, max_len, rows, (uint64_t)HD * 2,
-            (uint64_t)max_len * HD * 2, TC_KEYS, 1))
+            (uint64_t)max_len * HD * 2, kbox, 1))
     return -1;
   static uint64_t attr = 0;
   int dev = 0;
@@ -492,6 +793,17 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     return t;
   }();
   TcArgs args{pos, seq, (__nv_bfloat16*)out, T, H, KV, G, R, scale * 1.4426950408889634f, trace};
+  if (variant == 2) {
+    using P = PpCfg<HD>;
+    static uint64_t pattr = 0;
+    if (!(pattr >> dev & 1)) {
+      LP_CUDA(cudaFuncSetAttribute(attention_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
+      pattr |= 1ull << dev;
+    }
+    const dim3 grid((unsigned)((T + 2 * R - 1) / (2 * R)), (unsigned)KV);
+    LP_CUDA(lp::launch(attention_pp_kernel<HD>, grid, dim3(PP_THREADS), P::SMEM, s, mq, mk, mv, args));
+    return 0;
+  }
   const dim3 grid((unsigned)((T + R - 1) / R), (unsigned)KV);
   LP_CUDA(lp::launch(attention_tc_kernel<HD>, grid, dim3(TC_THREADS), C::SMEM, s, mq, mk, mv, args));
   if (trace) {
