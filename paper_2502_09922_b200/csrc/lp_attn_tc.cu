@@ -564,42 +564,48 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         run(lo, hi, sq, nch);
         total += nch;
       }
-      auto issue_pv = [&](int j) {
+      auto issue_pv = [&](int t, int j) {
         const int b = j & 1;
-        lp::mbar_wait(&v_full[b], (j >> 1) & 1);
+        if (t == 0) lp::mbar_wait(&v_full[b], (j >> 1) & 1);
+        lp::mbar_wait(&p_full[t][b], (j >> 1) & 1);
+        fence_after();
         const uint32_t sv = lp::smem_u32(sm + C::OFF_V + b * C::KV_BYTES);
-        for (int t = 0; t < 2; ++t) {
-          lp::mbar_wait(&p_full[t][b], (j >> 1) & 1);
-          fence_after();
-          const uint32_t sp = lp::smem_u32(sm + C::OFF_P + (t * 2 + b) * C::P_BYTES);
+        const uint32_t sp = lp::smem_u32(sm + C::OFF_P + (t * 2 + b) * C::P_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < PP_KEYS / 16; ++kk)
-            umma(tmem + t * C::TILE_COLS + 128, desc_sw128(sp + kk * 32, 16, 1024),
-                 desc_sw128(sv + kk * 2048, PP_KEYS * 128, 1024), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-          commit(&o_done[t]);
-        }
-        commit(&v_empty[b]);
+        for (int kk = 0; kk < PP_KEYS / 16; ++kk)
+          umma(tmem + t * C::TILE_COLS + 128, desc_sw128(sp + kk * 32, 16, 1024),
+               desc_sw128(sv + kk * 2048, PP_KEYS * 128, 1024), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        commit(&o_done[t]);
+        if (t == 1) commit(&v_empty[b]);
       };
+      auto issue_s = [&](int t, int it) {
+        const int st = it & 1;
+        if (it >= 2) lp::mbar_wait(&s_empty[t][st], ((it >> 1) - 1) & 1);
+        fence_after();
+        const uint32_t sk = lp::smem_u32(sm + C::OFF_K + st * C::KV_BYTES);
+        const uint32_t sq = lp::smem_u32(sm + C::OFF_Q + t * C::Q_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma(tmem + t * C::TILE_COLS + st * PP_KEYS, desc_sw128(sq + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
+               desc_sw128(sk + (kk >> 2) * (PP_KEYS * 128) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
+        commit(&s_full[t][st]);
+        if (t == 1) commit(&k_empty[st]);
+      };
+      // ping-pong order: tile 1's S of chunk it waits for tile 0's P of the
+      // previous chunk, which keeps the two softmax warpgroups half a period
+      // apart (one in the SFU-heavy exp phase while the other loads / reduces)
       lp::mbar_wait(&q_full, 0);
       for (int it = 0; it < total; ++it) {
-        const int st = it & 1;
-        lp::mbar_wait(&k_full[st], (it >> 1) & 1);
-        const uint32_t sk = lp::smem_u32(sm + C::OFF_K + st * C::KV_BYTES);
-        for (int t = 0; t < 2; ++t) {
-          if (it >= 2) lp::mbar_wait(&s_empty[t][st], ((it >> 1) - 1) & 1);
-          fence_after();
-          const uint32_t sq = lp::smem_u32(sm + C::OFF_Q + t * C::Q_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk)
-            umma(tmem + t * C::TILE_COLS + st * PP_KEYS,
-                 desc_sw128(sq + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
-                 desc_sw128(sk + (kk >> 2) * (PP_KEYS * 128) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
-          commit(&s_full[t][st]);
-        }
-        commit(&k_empty[st]);
-        if (it > 0) issue_pv(it - 1);
+        lp::mbar_wait(&k_full[it & 1], (it >> 1) & 1);
+        issue_s(0, it);
+        if (it > 0) issue_pv(0, it - 1);
+        issue_s(1, it);
+        if (it > 0) issue_pv(1, it - 1);
       }
-      if (total > 0) issue_pv(total - 1);
+      if (total > 0) {
+        issue_pv(0, total - 1);
+        issue_pv(1, total - 1);
+      }
     }
   } else if (warp <= 9) {
     // ---------------- softmax: warpgroup t owns Q tile t, thread = row ----------------
