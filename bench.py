@@ -379,6 +379,7 @@ def main():
     ap.add_argument("--no-serving-70b", action="store_true")
     ap.add_argument("--burst-compress", type=float, default=60.0)
     args = ap.parse_args()
+    t_start = time.perf_counter()
     global POISON
     POISON = not args.no_poison
     if args.impl == "reference":
@@ -635,6 +636,7 @@ def main():
             line["execute_while_load_70b"] = serving70
         if burst:
             line["bursty_trace"] = burst
+        line["bench_wall_s"] = round(time.perf_counter() - t_start, 1)
         print(json.dumps(line), flush=True)
     if distributed:
         dist.barrier()
