@@ -597,6 +597,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       lp::mbar_wait(&q_full, 0);
       for (int it = 0; it < total; ++it) {
         lp::mbar_wait(&k_full[it & 1], (it >> 1) & 1);
+        TRACE(0, it);
         issue_s(0, it);
         if (it > 0) issue_pv(0, it - 1);
         issue_s(1, it);
@@ -625,6 +626,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         const int b = it & 1;
         lp::mbar_wait(&s_full[t][b], (it >> 1) & 1);
         fence_after();
+        if ((warp == 2 || warp == 6) && lane == 0) TRACE(2 + 4 * t, it);
         const int lim = mine ? prow - c * PP_KEYS : -1;     // keys 0..lim of this chunk are visible
         uint32_t v[64];
         ld32(trow + b * PP_KEYS, *reinterpret_cast<uint32_t(*)[32]>(v));
@@ -633,6 +635,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[t][b]);
+        if ((warp == 2 || warp == 6) && lane == 0) TRACE(3 + 4 * t, it);
         float mx8[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
@@ -667,6 +670,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           }
           wait_st();
         }
+        if ((warp == 2 || warp == 6) && lane == 0) TRACE(4 + 4 * t, it);
         float ls[4] = {0.f, 0.f, 0.f, 0.f};
         uint8_t* prow_s = sm + C::OFF_P + (t * 2 + b) * C::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
         if (lim < 0) {
@@ -698,6 +702,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t][b]);
+        if ((warp == 2 || warp == 6) && lane == 0) TRACE(5 + 4 * t, it);
       }
     }
     if (it > 0) {
@@ -801,6 +806,7 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   TcArgs args{pos, seq, (__nv_bfloat16*)out, T, H, KV, G, R, scale * 1.4426950408889634f, trace};
   if (variant == 2) {
     using P = PpCfg<HD>;
+    if (trace) LP_CUDA(cudaMemset(trace, 0, 64 * 16 * sizeof(long long)));
     static uint64_t pattr = 0;
     if (!(pattr >> dev & 1)) {
       LP_CUDA(cudaFuncSetAttribute(attention_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
@@ -808,6 +814,17 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     }
     const dim3 grid((unsigned)((T + 2 * R - 1) / (2 * R)), (unsigned)KV);
     LP_CUDA(lp::launch(attention_pp_kernel<HD>, grid, dim3(PP_THREADS), P::SMEM, s, mq, mk, mv, args));
+    if (trace) {
+      static long long h[64 * 16];
+      LP_CUDA(cudaStreamSynchronize(s));
+      LP_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
+      for (int it = 0; it < 64 && h[it * 16]; ++it) {
+        const long long* t = h + it * 16;
+        fprintf(stderr, "pp chunk %2d: K_ready %7lld | tile0 S_ready %7lld ld %+5lld max %+5lld P %+5lld | tile1 S_ready "
+                "%7lld ld %+5lld max %+5lld P %+5lld\n", it, t[0] - h[0], t[2] - h[0], t[3] - t[2], t[4] - t[3],
+                t[5] - t[4], t[6] - h[0], t[7] - t[6], t[8] - t[7], t[9] - t[8]);
+      }
+    }
     return 0;
   }
   const dim3 grid((unsigned)((T + R - 1) / R), (unsigned)KV);
