@@ -157,7 +157,9 @@ int lp_mc_node_ops(lp_mc* mc, int node, int* kernel_ops, int* dma_ops);
 /* tunables: "wide_loads" (0/1: 256 B L2 fetch granule on LDG-role loads),
  * "window" (1..8), "timeout_ms" (flag-wait watchdog, default 20000),
  * "host_dma" (0/1: HOST-sourced transfers on the copy engines, see
- * lp_mc_run_host_dma) */
+ * lp_mc_run_host_dma), "ce_split" (m >= 0: GPU->GPU transfers of blocks with
+ * block % m == 0 also leave the kernel for lp_mc_run_host_dma's copy-engine
+ * list, so DMA engines and SMs share every link; 0 = off) */
 int lp_mc_set_option(lp_mc* mc, const char* name, int64_t value);
 /* synchronise `stream`; code = 1 (and return -3) if a flag wait timed out */
 int lp_mc_status(lp_mc* mc, void* stream, int* code);

@@ -471,6 +471,7 @@ struct lp_mc {
   int window = 3;
   int wide_loads = 0;
   int host_dma = 0;                   // HOST-sourced transfers run on the copy engines (lp_mc_run_host_dma)
+  int ce_split = 0;                   // > 0: GPU-sourced transfers of blocks b % ce_split == 0 run there too
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;   // flag-wait watchdog
   uint32_t last_epoch = 0;            // last epoch launched on this handle
   bool failed = false;                // a watchdog expired: signals must be reset before the next run
@@ -535,7 +536,11 @@ static int compile(lp_mc* mc) {
   auto pulled = [&](const Row& r) { return mc->direction == 1 || from_host(r); };
   // with host_dma the receiver's copy engine performs the PCIe hop and the
   // kernel only relays over NVLink (waiting on the flags the DMA publishes)
-  auto dma = [&](const Row& r) { return mc->host_dma && from_host(r); };
+  // with ce_split = m, GPU->GPU transfers of every m-th block also go to the
+  // copy engines, so DMA engines and SMs share each link's traffic
+  auto dma = [&](const Row& r) {
+    return (mc->host_dma && from_host(r)) || (mc->ce_split > 0 && !from_host(r) && r.blk % mc->ce_split == 0);
+  };
   std::vector<OpDev> ops;
   std::vector<int32_t> recv;
   mc->per_node.assign(N, ExecDesc{});
@@ -544,7 +549,8 @@ static int compile(lp_mc* mc) {
     d.node = n;
     d.push_b = (int)ops.size();
     for (const Row& r : rows)
-      if (r.snd == n && !pulled(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1, r.step, 0});
+      if (r.snd == n && !pulled(r) && !dma(r))
+        ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1, r.step, 0});
     d.push_e = (int)ops.size();
     d.pull_b = (int)ops.size();
     for (const Row& r : rows)
@@ -553,12 +559,12 @@ static int compile(lp_mc* mc) {
     d.pull_e = (int)ops.size();
     d.dma_b = (int)ops.size();
     for (const Row& r : rows)
-      if (r.rcv == n && dma(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, 0, r.step, 0});
+      if (r.rcv == n && dma(r)) ops.push_back(OpDev{r.blk, r.snd, r.rcv, is_src[r.snd] ? 0 : 1, r.step, 0});
     d.dma_e = (int)ops.size();
     // tiles other nodes push into n: waited for before n's kernel completes
     d.recv_b = (int)recv.size();
     for (const Row& r : rows)
-      if (r.rcv == n && !pulled(r)) recv.push_back(r.blk);
+      if (r.rcv == n && !pulled(r) && !dma(r)) recv.push_back(r.blk);
     d.recv_e = (int)recv.size();
   }
   // receive order per node (verify kernel): blocks in the step order they land
@@ -713,6 +719,10 @@ int lp_mc_set_option(lp_mc* mc, const char* name, int64_t value) {
   } else if (!strcmp(name, "window")) {
     LP_CHECK(value >= 1 && value <= kMaxWindow, "lp_mc_set_option: window must be in [1, %d]", kMaxWindow);
     mc->window = (int)value;
+  } else if (!strcmp(name, "ce_split")) {
+    LP_CHECK(value >= 0 && value <= 64, "lp_mc_set_option: ce_split must be in [0, 64]");
+    if (value != mc->ce_split) mc->dirty = true;
+    mc->ce_split = (int)value;
   } else if (!strcmp(name, "host_dma")) {
     if ((value != 0) != (mc->host_dma != 0)) mc->dirty = true;
     mc->host_dma = value != 0;
@@ -897,7 +907,7 @@ int lp_mc_run_host_dma(lp_mc* mc, int node, uint32_t epoch, int n_streams, void*
   if (resolve_stream_memops() != 0) return -1;
   LP_CHECK(mc && node >= 0 && node < mc->n_nodes, "lp_mc_run_host_dma: bad node");
   LP_CHECK(epoch >= 1 && n_streams >= 1 && streams, "lp_mc_run_host_dma: bad arguments");
-  LP_CHECK(mc->host_dma, "lp_mc_run_host_dma: enable option host_dma first");
+  LP_CHECK(mc->host_dma || mc->ce_split, "lp_mc_run_host_dma: enable option host_dma or ce_split first");
   if (mc->dirty && compile(mc) != 0) return -2;
   const ExecDesc ex = mc->per_node[node];
   std::vector<int> seq;

@@ -387,13 +387,18 @@ class ScaleOut:
             n_gpu = len(plan.nodes) - (1 if plan.host_source else 0)
             self.cluster = E.Cluster.local(n_gpu, lay.block_offsets, lay.block_lengths, lay.weights_bytes,
                                            device=device, host_node=plan.host_source, tile_bytes=tile_bytes)
-        if executor not in ("kernel", "ce", "hybrid"):
+        if executor not in ("kernel", "ce", "hybrid", "split"):
             raise ValueError("executor is 'kernel' (in-kernel NVLink/PCIe copies), 'ce' (copy engines), "
-                             "'hybrid' (host DMA + in-kernel relay) or 'auto'")
+                             "'hybrid' (host DMA + in-kernel relay), 'split' (hybrid + every other block's "
+                             "GPU->GPU transfers on the copy engines) or 'auto'")
+        self.split = executor == "split"
+        if self.split:
+            executor = "hybrid"
         self.executor = executor
         self.ce_streams = ce_streams
         self.cluster.engine.configure(direction, copy_mode, copy_mode, chunk_bytes, 3)
         self.cluster.engine.set_option("host_dma", int(executor == "hybrid"))
+        self.cluster.engine.set_option("ce_split", 2 if self.split else 0)
         self.kernel_launches = 0      # multicast kernels of the last run (this process)
         # verify-as-it-lands (lp_mc_verify): receivers checksum every block
         # once its counter completes (one checksum launch per block, grid

@@ -35,6 +35,9 @@ def want():
     (3, 1, 4, True, "kernel", 1 << 20),
     (3, 1, 4, True, "ce", 1 << 20),
     (4, 2, 3, False, "kernel", 4096 * 16),
+    (4, 1, 4, False, "split", 1 << 20),
+    (5, 2, 4, False, "split", 64 * 1024),
+    (5, 1, 4, True, "split", 1 << 20),
 ])
 def test_scale_out_verifies_while_landing(n, k, b, host, executor, tile, want):
     plan = SO.plan_scale_out("tiny", n, k=k, block_count=b, host_source=host)
