@@ -36,6 +36,7 @@ from . import engine as E
 from .cluster import AutoscalePolicy, autoscale
 from .image import CONFIGS, build_layout, model_spec
 from .pipeline import plan_mode_switch
+from .errors import UnsatisfiableScalingError
 from .modelmgr import TierMap
 from .scaleout import CE_TILE, plan_from_tiers
 from .serving import Request, Server, Stage
@@ -151,7 +152,7 @@ class AutoscaleServer(Server):
         try:
             tp = plan_from_tiers(self.cfg, targets, self.tiers(), k=self.k, block_count=self.lay.plan.block_count,
                                  host_id=self.host_id)
-        except Exception:     # noqa: BLE001  (no copy anywhere: UnsatisfiableScalingError)
+        except UnsatisfiableScalingError:     # no copy of the model anywhere: nothing to scale from
             return
         if tp.plan is None:
             return
