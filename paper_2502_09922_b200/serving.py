@@ -12,7 +12,8 @@ GPU), receivers that hold only their pipeline stage's blocks already serve:
   norm, LM head) for the next token.  A unit activates when every block its
   stages need has *landed* (the engine's per-block tile counters) — the
   measured counterpart of ``activation_step`` (pipeline.py:175-185);
-* capacity = stage count (pipeline.py:43-46); requests are admitted FIFO into
+* capacity = stage count (pipeline.py:43-46; × ``pipeline_batch`` requests
+  per slot when local replicas batch too); requests are admitted FIFO into
   free slots of active units in unit order (``_admit``, simengine.py:356-368)
   and batched per iteration (prefill and decode tokens in one ragged batch);
 * when every receiver holds the whole model the pipelines retire and
@@ -105,7 +106,14 @@ class Server:
     """Serves a request trace while ``plan`` is being multicast."""
 
     def __init__(self, plan, cluster, local_slots: int = 8, max_len: int = 512, switch_hold_tokens: int = 0,
-                 prefill_ms_per_token: float = 0.5, use_graphs: bool = True):
+                 prefill_ms_per_token: float = 0.5, use_graphs: bool = True, pipeline_batch: int = 1):
+        """``pipeline_batch``: requests per pipeline slot.  The reference's
+        capacity is one request per stage (pipeline.py:43-46) — with its
+        one-request local units (``batch_slots = 1``, simengine.py:236).
+        Local replicas here batch ``local_slots`` requests; passing
+        ``pipeline_batch = local_slots`` scales the pipelines the same way
+        (capacity = stages x pipeline_batch), keeping the reference's ratio of
+        pipeline to local capacity."""
         import torch
         self.plan = plan
         self.cluster = cluster
@@ -116,6 +124,7 @@ class Server:
         self.switch_hold_tokens = switch_hold_tokens
         self.use_graphs = use_graphs
         self.prefill_ms_per_token = prefill_ms_per_token
+        self.pipeline_batch = max(1, int(pipeline_batch))
         self.events = []
         self.profile = []          # per iteration: (start, enqueue s, device s, tokens, unit batches)
         self.profile_detail = [] if os.environ.get("LP_SERVE_PROFILE") else None
@@ -140,7 +149,7 @@ class Server:
                 covered = max(covered, l_hi)
                 stages.append(Stage(st.node, cluster.node_device(st.node), st.block_lo, st.block_hi, l_lo, l_hi,
                                     st.block_lo == 0))
-            self._add_unit("pipeline", stages, max(1, len(ep.stages)), True, ep)
+            self._add_unit("pipeline", stages, max(1, len(stages)) * self.pipeline_batch, True, ep)
         # post-switch local replicas, built (and their decode graphs captured)
         # before the scale-out starts; activated at mode switch
         self.local_units = {n: self._local_unit(n, active=False) for n in self.receivers}
@@ -246,7 +255,9 @@ class Server:
             inflight = [u.busy[s] for s in sorted(u.busy)]
             plan = plan_mode_switch(u.pipeline, [(r.rid, len(r.out)) for r in inflight],
                                     self.prefill_ms_per_token)
-            locals_by_node = {n: self.local_units[n] for n in u.nodes}
+            # every node of the plan's pipeline (an empty stage's node too:
+            # plan_mode_switch deals requests over all of them)
+            locals_by_node = {st.node: self.local_units[st.node] for st in u.pipeline.stages}
             for lu in locals_by_node.values():
                 lu.active = True
             by_id = {r.rid: r for r in inflight}

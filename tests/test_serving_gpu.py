@@ -9,7 +9,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def test_execute_while_load_tiny_matches_oracle():
+@pytest.mark.parametrize("pipeline_batch", [1, 2])
+def test_execute_while_load_tiny_matches_oracle(pipeline_batch):
     import torch
     from paper_2502_09922_b200 import engine as E
     from paper_2502_09922_b200 import scaleout as SO
@@ -25,7 +26,8 @@ def test_execute_while_load_tiny_matches_oracle():
         for s in plan.sources:
             E.load_source_image(cl, s, lay, 7)
         cl.set_schedule_all(plan.schedule, plan.sources)
-        srv = Server(plan, cl, local_slots=4, max_len=64, switch_hold_tokens=6)
+        srv = Server(plan, cl, local_slots=4, max_len=64, switch_hold_tokens=6, pipeline_batch=pipeline_batch)
+        assert srv.units[0].slots == 2 * pipeline_batch
         from parity import assert_tokens, doc
         es = {f"r{i}": e for i, e in enumerate(e for e in doc()["prompts"] if len(e["prompt"]) in (10, 11, 12))}
         prompts = {rid: e["prompt"] for rid, e in es.items()}

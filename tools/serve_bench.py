@@ -20,7 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int = 16, requests: int = 16,
                 prompt_len: int = 128, out_tokens: int = 32, spacing_s: float = 0.001, pull_ctas: int = 32,
                 local_slots: int = 16, seed: int = 20250815, executor: str = "ce", outdir: str | None = None,
-                node_devices: list | None = None, host_source: bool = False):
+                node_devices: list | None = None, host_source: bool = False, pipeline_batch: int | None = None):
     """host_source: the tier-driven plan (scaleout.plan_from_tiers) with GPU 0
     holding the model and the box's pinned host copy as the second source
     (k = 2): one sub-group is fed over PCIe, GPUs 1..n-1 are cold."""
@@ -54,7 +54,9 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         for d in devs:
             cl.per_device[d].configure(1, 0, 0, 16384, 3)
         graphs = not os.environ.get("LP_NO_GRAPHS")
-        srv = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs)
+        pb = local_slots if pipeline_batch is None else pipeline_batch
+        srv = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs,
+                     pipeline_batch=pb)
         rng = np.random.default_rng(seed)
         prompts = {f"r{i}": rng.integers(0, plan.config.vocab, prompt_len).tolist() for i in range(requests)}
         trace = [TraceRecord(f"r{i}", spacing_s * i, model, prompt_len, out_tokens) for i in range(requests)]
@@ -62,7 +64,8 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         # warm-up (kernels, allocator, tensor maps): a tiny burst on a second epoch is not needed;
         # run one short pass first and report the second
         srv.run(trace[:2], prompts, streams, pull_ctas=pull_ctas, executor=executor)
-        srv2 = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs)
+        srv2 = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs,
+                      pipeline_batch=pb)
         ev = srv2.run(trace, prompts, streams, pull_ctas=pull_ctas, executor=executor)
         rep = aggregate(ev, "lambda_scale")
         if outdir:   # the reference's result files: `blockcast report <outdir>` re-aggregates them
@@ -92,7 +95,8 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         return {
             "multicast_executor": executor + (" (push direction: one process drives every GPU, DESIGN §5.1)" if executor == "ce" else ""),
             "workload": f"{model} bf16, sources {plan.sources} (HOST positions {list(plan.host_nodes)}), "
-                        f"receivers {plan.receivers}, b={blocks}, k={k}; "
+                        f"receivers {plan.receivers}, b={blocks}, k={k}, pipeline capacity stages x {pb}, "
+                        f"local replicas {local_slots} slots; "
                         f"{requests} requests x (prompt {prompt_len}, out {out_tokens}), {spacing_s * 1e3:.0f} ms apart at t=0",
             "pipelines": [[(st.node, st.block_lo, st.block_hi) for st in ep.stages] for ep in plan.pipelines],
             "pipeline_activation_s": sorted(srv2.activation_s.values()),
@@ -124,8 +128,10 @@ if __name__ == "__main__":
     ap.add_argument("--outdir", default=None, help="write the reference's result files (cli.py:268-281) here")
     ap.add_argument("--node-devices", default="", help="comma list: GPU of each schedule node (default 0..gpus-1)")
     ap.add_argument("--host-source", action="store_true", help="GPU 0 + the pinned host copy as the k = 2 sources")
+    ap.add_argument("--pipeline-batch", type=int, default=None,
+                    help="requests per pipeline slot (default = local slots; 1 = the reference's capacity)")
     a = ap.parse_args()
     print(json.dumps(run_serving(a.gpus, a.model, a.k, a.blocks, a.requests, out_tokens=a.out_tokens,
                                  executor=a.executor, pull_ctas=a.pull_ctas, outdir=a.outdir,
                                  node_devices=[int(x) for x in a.node_devices.split(",")] if a.node_devices else None,
-                                 host_source=a.host_source)))
+                                 host_source=a.host_source, pipeline_batch=a.pipeline_batch)))
