@@ -272,6 +272,21 @@ def block_checksums(device_ptr: int, offsets, lengths, stream: int = 0) -> list:
     return list(out)
 
 
+def _fit_ctas(device: int, n_exec: int, push_ctas: int, pull_ctas: int) -> tuple:
+    """Scale per-node CTA counts so ``n_exec`` nodes fit one CTA per SM."""
+    import torch
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    per = push_ctas + pull_ctas
+    if n_exec * per <= sms:
+        return push_ctas, pull_ctas
+    room = max(1, sms // max(1, n_exec))
+    push = (push_ctas * room) // per if push_ctas else 0
+    pull = room - push if pull_ctas else 0
+    if push_ctas and push == 0:
+        push, pull = 1, max(0, room - 1) if pull_ctas else 0
+    return push, pull
+
+
 class Cluster:
     """Node images addressable from this process + the engine that moves them."""
 
@@ -432,8 +447,11 @@ class Cluster:
         streams = self._mc_streams
         for d, eng in self.per_device.items():
             mine = [nb.node for nb in self.nodes if nb.kind == LP_NODE_GPU and nb.device == d]
+            # every CTA of the dataflow must be co-resident: several nodes on
+            # one device (tests, host-fed boxes) share its SMs
+            push, pull = _fit_ctas(d, len(mine), push_ctas, pull_ctas)
             with on_device(d):
-                eng.run(mine, self.epoch, push_ctas, pull_ctas, streams[d])
+                eng.run(mine, self.epoch, push, pull, streams[d])
         return self.epoch
 
     def launch_devices_ce(self, streams: dict) -> int:

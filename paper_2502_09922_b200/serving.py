@@ -106,14 +106,21 @@ class Server:
     """Serves a request trace while ``plan`` is being multicast."""
 
     def __init__(self, plan, cluster, local_slots: int = 8, max_len: int = 512, switch_hold_tokens: int = 0,
-                 prefill_ms_per_token: float = 0.5, use_graphs: bool = True, pipeline_batch: int = 1):
+                 prefill_ms_per_token: float = 0.5, use_graphs: bool = True, pipeline_batch: int = 1,
+                 pipeline_prefill_tokens: int = 256):
         """``pipeline_batch``: requests per pipeline slot.  The reference's
         capacity is one request per stage (pipeline.py:43-46) — with its
         one-request local units (``batch_slots = 1``, simengine.py:236).
         Local replicas here batch ``local_slots`` requests; passing
         ``pipeline_batch = local_slots`` scales the pipelines the same way
         (capacity = stages x pipeline_batch), keeping the reference's ratio of
-        pipeline to local capacity."""
+        pipeline to local capacity.
+
+        ``pipeline_prefill_tokens``: prompt tokens a pipeline pass prefills
+        (at least one request; the rest keep waiting in their slots, decodes
+        always run).  Without it a burst admitted into a wide pipeline is one
+        long prefill that pushes every first token past the first full
+        replica."""
         import torch
         self.plan = plan
         self.cluster = cluster
@@ -125,6 +132,7 @@ class Server:
         self.use_graphs = use_graphs
         self.prefill_ms_per_token = prefill_ms_per_token
         self.pipeline_batch = max(1, int(pipeline_batch))
+        self.pipeline_prefill_tokens = max(1, int(pipeline_prefill_tokens))
         self.events = []
         self.profile = []          # per iteration: (start, enqueue s, device s, tokens, unit batches)
         self.profile_detail = [] if os.environ.get("LP_SERVE_PROFILE") else None
@@ -355,6 +363,16 @@ class Server:
                     reqs = []
             if not reqs:
                 return out
+        if u.kind == "pipeline":
+            keep, n_pf = [], 0
+            for r in reqs:
+                if r.needs_prefill:
+                    n = len(r.prompt) + len(r.out)
+                    if n_pf and n_pf + n > self.pipeline_prefill_tokens:
+                        continue
+                    n_pf += n
+                keep.append(r)
+            reqs = keep
         tokens, pos, seq, last = [], [], [], []
         for r in reqs:
             if r.needs_prefill:

@@ -9,8 +9,10 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("pipeline_batch", [1, 2])
-def test_execute_while_load_tiny_matches_oracle(pipeline_batch):
+@pytest.mark.parametrize("pipeline_batch,prefill_tokens", [(1, 256), (2, 256), (2, 1)])
+def test_execute_while_load_tiny_matches_oracle(pipeline_batch, prefill_tokens):
+    """prefill_tokens = 1: one prefill per pipeline pass, the other admitted
+    requests wait in their slots while the first one decodes."""
     import torch
     from paper_2502_09922_b200 import engine as E
     from paper_2502_09922_b200 import scaleout as SO
@@ -26,7 +28,8 @@ def test_execute_while_load_tiny_matches_oracle(pipeline_batch):
         for s in plan.sources:
             E.load_source_image(cl, s, lay, 7)
         cl.set_schedule_all(plan.schedule, plan.sources)
-        srv = Server(plan, cl, local_slots=4, max_len=64, switch_hold_tokens=6, pipeline_batch=pipeline_batch)
+        srv = Server(plan, cl, local_slots=4, max_len=64, switch_hold_tokens=6, pipeline_batch=pipeline_batch,
+                     pipeline_prefill_tokens=prefill_tokens)
         assert srv.units[0].slots == 2 * pipeline_batch
         from parity import assert_tokens, doc
         es = {f"r{i}": e for i, e in enumerate(e for e in doc()["prompts"] if len(e["prompt"]) in (10, 11, 12))}
