@@ -107,7 +107,7 @@ class Server:
 
     def __init__(self, plan, cluster, local_slots: int = 8, max_len: int = 512, switch_hold_tokens: int = 0,
                  prefill_ms_per_token: float = 0.5, use_graphs: bool = True, pipeline_batch: int = 1,
-                 pipeline_prefill_tokens: int = 256):
+                 pipeline_prefill_tokens: int = 512):
         """``pipeline_batch``: requests per pipeline slot.  The reference's
         capacity is one request per stage (pipeline.py:43-46) — with its
         one-request local units (``batch_slots = 1``, simengine.py:236).

@@ -20,8 +20,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int = 16, requests: int = 16,
                 prompt_len: int = 128, out_tokens: int = 32, spacing_s: float = 0.001, pull_ctas: int = 32,
                 local_slots: int = 16, seed: int = 20250815, executor: str = "ce", outdir: str | None = None,
-                node_devices: list | None = None, host_source: bool = False, pipeline_batch: int = 1,
-                pipeline_prefill_tokens: int = 256):
+                node_devices: list | None = None, host_source: bool = False, pipeline_batch: int | None = None,
+                pipeline_prefill_tokens: int = 512):
     """host_source: the tier-driven plan (scaleout.plan_from_tiers) with GPU 0
     holding the model and the box's pinned host copy as the second source
     (k = 2): one sub-group is fed over PCIe, GPUs 1..n-1 are cold."""
@@ -55,7 +55,7 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
         for d in devs:
             cl.per_device[d].configure(1, 0, 0, 16384, 3)
         graphs = not os.environ.get("LP_NO_GRAPHS")
-        pb = pipeline_batch
+        pb = local_slots if pipeline_batch is None else pipeline_batch
         srv = Server(plan, cl, local_slots=local_slots, max_len=prompt_len + out_tokens + 8, use_graphs=graphs,
                      pipeline_batch=pb, pipeline_prefill_tokens=pipeline_prefill_tokens)
         rng = np.random.default_rng(seed)
@@ -129,10 +129,9 @@ if __name__ == "__main__":
     ap.add_argument("--outdir", default=None, help="write the reference's result files (cli.py:268-281) here")
     ap.add_argument("--node-devices", default="", help="comma list: GPU of each schedule node (default 0..gpus-1)")
     ap.add_argument("--host-source", action="store_true", help="GPU 0 + the pinned host copy as the k = 2 sources")
-    ap.add_argument("--pipeline-batch", type=int, default=1,
-                    help="requests per pipeline slot (1 = the reference's capacity; larger batches delay the "
-                         "first token, profiles/r02/README.md)")
-    ap.add_argument("--pipeline-prefill-tokens", type=int, default=256,
+    ap.add_argument("--pipeline-batch", type=int, default=None,
+                    help="requests per pipeline slot (default = local slots; 1 = the reference's capacity)")
+    ap.add_argument("--pipeline-prefill-tokens", type=int, default=512,
                     help="prompt tokens one pipeline pass prefills (serving.Server)")
     a = ap.parse_args()
     print(json.dumps(run_serving(a.gpus, a.model, a.k, a.blocks, a.requests, out_tokens=a.out_tokens,
