@@ -20,7 +20,10 @@
 // more than 2^8 (P then stays <= 256, exact enough in fp16; the row sum l
 // uses the same m), so O almost never needs rescaling: when it does, the
 // row's softmax threads rescale it in TMEM (after the previous P V) before
-// releasing P_j.  Final: O / l.
+// releasing P_j.  Final: O / l.  The default (lazy) variant computes P_j with
+// the current m first and only then combines the halves' raw maxima (one
+// atomicMax slot + a 64-thread named barrier per chunk), recomputing P_j from
+// the S values still in registers when m has to move.
 //
 //   warp 0   : TMA producer (Q once, then K chunks)      warp 10: TMA (V chunks)
 //   warp 1   : TMEM allocator + MMA issuer (one thread)
@@ -37,7 +40,7 @@ namespace {
 
 constexpr int TC_M = 128;       // rows per tile (TMEM lanes)
 constexpr int TC_KEYS = 128;    // keys per chunk
-constexpr int TC_THREADS = 352;   // warp 0 TMA (Q, K), warp 1 MMA, warps 2-9 softmax, warp 10 TMA (V)
+// threads: warp 0 TMA (Q, K), warp 1 MMA, 4 NS softmax warps, then one TMA (V) warp: (3 + 4 NS) x 32
 constexpr int ATOM = TC_M * 128;   // bytes of one 128-row x 128-byte swizzle column block
 
 template <int HD>
@@ -50,7 +53,10 @@ struct TcCfg {
   static constexpr int OFF_K = OFF_Q + Q_BYTES;         // 2 stages
   static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;    // 2 stages
   static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;    // 2 buffers
-  static constexpr int SMEM = OFF_P + 2 * P_BYTES + 1024;
+  static constexpr int BODY = OFF_P + 2 * P_BYTES;
+  // + the pad that aligns the body to 1024 B after the kernel's static smem
+  // (launch_tc computes it; the full 1024 B slack would not fit in 227 KB)
+
   static constexpr int S_COL = 0;                       // S buffers: [0, 128), [128, 256), [256, 384)
   static constexpr int O_COL = 3 * TC_KEYS;             // O accumulator: [384, 384 + HD)
 };
@@ -130,23 +136,78 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Packed fp32 pairs (Blackwell FFMA2 / FADD2: one issue slot for two lanes'
+// worth of math) and the 3-input max (FMNMX3)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (offloads the SFU, 16 ex2 / clock / SM on
+// B200 = the MMA time of a chunk): x = n + f with n = rint(x) via the
+// 1.5 * 2^23 magic add, f in [-0.5, 0.5], 2^f by a degree-3 fit (max relative
+// error 7.5e-5, below fp16 P's half ulp), n added to the exponent with one
+// IMAD.  x is clamped at -100 (2^-100 is 0 in fp16 P and in the row sum).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  constexpr float MAGIC = 12582912.0f;
+  x.x = fmaxf(x.x, -100.f);
+  x.y = fmaxf(x.y, -100.f);
+  const float2 t = fadd2(x, make_float2(MAGIC, MAGIC));
+  const float2 n = fadd2(t, make_float2(-MAGIC, -MAGIC));
+  const float2 f = fadd2(x, make_float2(-n.x, -n.y));
+  float2 q = ffma2(f, make_float2(0.05517166f, 0.05517166f), make_float2(0.24261116f, 0.24261116f));
+  q = ffma2(q, f, make_float2(0.69326099f, 0.69326099f));
+  q = ffma2(q, f, make_float2(0.99992807f, 0.99992807f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+// order-preserving int image of a float (atomicMax on floats of any sign)
+constexpr int ORD_NEG_INF = (int)0x807FFFFF;   // ord_f32(-inf)
+__device__ __forceinline__ int ord_f32(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float unord_f32(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lp::smem_u32(bar)) : "memory");
 }
 
-template <int HD>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <int HD, int NS, bool LAZY, int POLY = 1>
+__global__ void __launch_bounds__((3 + 4 * NS) * 32, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const TcArgs a) {
   using C = TcCfg<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  if (threadIdx.x == 0) {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if ((uint32_t)(sm - smem_raw) + C::BODY > dyn) __trap();   // launch_tc's pad assumption broken
+  }
   __shared__ __align__(8) uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[3], s_empty[3],
-      p_full[2], o_done;
+      p_full[2], o_done, o_final;
   __shared__ uint32_t tmem_base;
   __shared__ int s_pos[TC_M];                 // per token of the tile (-1 past T)
   __shared__ int16_t s_seq[TC_M];
-  __shared__ float s_mx[2][TC_M];              // row max / row sum exchange between column halves
+  __shared__ int s_cmx[3][TC_M];               // lazy path: joint raw row max per chunk (it % 3)
+  static_assert(NS == 2 || (LAZY && HD % (32 * NS) == 0), "4-way key split: lazy path, 32 O columns per warp");
+  constexpr int VW = 2 + 4 * NS;               // the V producer warp (after the softmax warps)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = gridDim.x - 1 - blockIdx.x;          // later (longer) tiles first: causal balance
   const int kh = blockIdx.y;
@@ -159,13 +220,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       lp::mbar_init(&k_empty[b], 1);
       lp::mbar_init(&v_full[b], 1);
       lp::mbar_init(&v_empty[b], 1);
-      lp::mbar_init(&p_full[b], 8);
+      lp::mbar_init(&p_full[b], 4 * NS);
     }
     for (int b = 0; b < 3; ++b) {
       lp::mbar_init(&s_full[b], 1);
-      lp::mbar_init(&s_empty[b], 8);
+      lp::mbar_init(&s_empty[b], 4 * NS);
     }
     lp::mbar_init(&o_done, 1);
+    lp::mbar_init(&o_final, 1);
     lp::fence_mbar_init();
   }
   if (warp == 1) {
@@ -182,6 +244,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   lp::pdl_wait();
   lp::pdl_trigger();
   // token table and sequence runs of the tile
+  for (int i = threadIdx.x; i < 3 * TC_M; i += blockDim.x) (&s_cmx[0][0])[i] = ORD_NEG_INF;
   for (int i = threadIdx.x; i < a.R; i += blockDim.x) {
     const bool v = t0 + i < a.T;
     s_pos[i] = v ? a.pos[t0 + i] : -1;
@@ -200,7 +263,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   };
   const int nvalid = min(a.R, a.T - t0);
 
-  if (warp == 0 || warp == 10) {
+  if (warp == 0 || warp == VW) {
     if (lane == 0) {
       // ---------------- TMA producers: warp 0 Q + K, warp 10 V ----------------
       // K_j's stage frees when S_j is done, V_j's when P_j V_j is: separate
@@ -274,19 +337,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         commit(&k_empty[st]);
         if (it > 0) issue_pv(it - 1);
       }
-      if (total > 0) issue_pv(total - 1);
+      if (total > 0) {
+        issue_pv(total - 1);
+        commit(&o_final);      // every MMA done: o_done's parity cannot tell phase it-1 from it-3
+      }
     }
-  } else if (warp <= 9) {
+  } else if (warp < VW) {
     // ---------------- softmax ----------------
     // two warps per TMEM lane quarter: thread (row r, half h) owns keys
     // [64h, 64h + 64) of every S chunk (= P atom h) and O columns
     // [h HD/2, (h + 1) HD/2); the row max is exchanged through smem once per
     // chunk (named barrier over the 256 softmax threads), the row sums only
     // at the end (both halves use the same m).
-    constexpr int HH = HD / 2;
+    constexpr int HH = HD / NS;                  // O columns per warp
     constexpr float RESCALE = 8.0f;              // log2 headroom before m moves (P <= 2^8 in fp16)
     const int quarter = warp & 3;
-    const int h = (warp - 2) >> 2;
+    const int hq = (warp - 2) >> 2;              // which NS-th of the keys / O columns
+    const int h = hq;
     const int r = quarter * 32 + lane;
     const int i = r / a.G, g = r % a.G;
     const int prow = i < nvalid ? s_pos[i] : -1;
@@ -301,6 +368,179 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         lp::mbar_wait(&s_full[sb], (it / 3) & 1);
         fence_after();
         if (warp == 2 && lane == 0) TRACE(2, it);
+        if constexpr (LAZY) {
+          // Lazy max: P is computed with the current m first, the row max
+          // (own keys, fused into the exp pass) is combined across the NS
+          // warps of the row through a shared atomicMax slot and one named
+          // barrier; only when the joint max moves m by more than RESCALE
+          // (first visible chunk, rare after) is P recomputed from the S
+          // values still in registers.
+          constexpr int KW = TC_KEYS / NS;             // keys of each chunk this warp owns
+          const int lim = mine ? prow - c * TC_KEYS - hq * KW : -1;
+          uint32_t v[KW];
+#pragma unroll
+          for (int cg = 0; cg < KW / 32; ++cg)
+            ld32(trow + C::S_COL + sb * TC_KEYS + hq * KW + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(v + cg * 32));
+          wait_ld();
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[sb]);
+          if (warp == 2 && lane == 0) TRACE(3, it);
+          uint8_t* prow_s = sm + C::OFF_P + b * C::P_BYTES + ((hq * KW) >> 6) * ATOM + (r >> 3) * 1024 + (r & 7) * 128;
+          const int cb = ((hq * KW) & 63) >> 3;       // my first 16-B chunk of the 128-B P row
+          // P (fp16) of my keys into smem with m = mu; returns the row sum;
+          // with want_max also the raw max over the visible keys.  Unmasked
+          // chunks (the whole warp below the diagonal) take packed math and
+          // send one key pair in four through the FMA-pipe exp2.
+          auto write_p = [&](float mu, float& mraw, auto want_max) -> float {
+            constexpr bool WM = decltype(want_max)::value;
+            const bool unmasked = __all_sync(0xffffffffu, lim >= KW - 1);   // before any lane returns
+            if (lim < 0) {
+#pragma unroll
+              for (int q = 0; q < KW / 8; ++q)
+                *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) = make_uint4(0, 0, 0, 0);
+              return 0.f;
+            }
+            const float nm = -mu;
+            if (unmasked) {
+              float2 ls2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+              float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+              const float2 sl = make_float2(a.sl2, a.sl2), nm2 = make_float2(nm, nm);
+#pragma unroll
+              for (int q = 0; q < KW / 8; ++q) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                  const int k = q * 8 + e;
+                  const float2 sv = make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1]));
+                  if (WM) mx4[e >> 1] = fmax3(mx4[e >> 1], sv.x, sv.y);
+                  const float2 x = ffma2(sv, sl, nm2);
+                  float2 p;
+                  if ((e >> 1) >= 4 - POLY) {      // POLY of every 4 key pairs on the FMA pipe
+                    p = exp2_poly2(x);
+                  } else {
+                    p.x = fast_exp2(x.x);
+                    p.y = fast_exp2(x.y);
+                  }
+                  ls2[e >> 1] = fadd2(ls2[e >> 1], p);
+                  const __half2 hv = __floats2half2_rn(p.x, p.y);
+                  pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+                }
+                *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) =
+                    make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              }
+              if (WM) mraw = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+              const float2 s01 = fadd2(ls2[0], ls2[1]), s23 = fadd2(ls2[2], ls2[3]);
+              return (s01.x + s01.y) + (s23.x + s23.y);
+            }
+            float ls[4] = {0.f, 0.f, 0.f, 0.f};
+            float mx8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < KW / 8; ++q) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                const int k = q * 8 + e;
+                const float s0 = __uint_as_float(v[k]), s1 = __uint_as_float(v[k + 1]);
+                float p0 = k <= lim ? fast_exp2(fmaf(s0, a.sl2, nm)) : 0.f;
+                float p1 = k + 1 <= lim ? fast_exp2(fmaf(s1, a.sl2, nm)) : 0.f;
+                if (WM) {
+                  mx8[e] = k <= lim ? fmaxf(mx8[e], s0) : mx8[e];
+                  mx8[e + 1] = k + 1 <= lim ? fmaxf(mx8[e + 1], s1) : mx8[e + 1];
+                }
+                ls[e >> 1] += p0 + p1;
+                const __half2 hv = __floats2half2_rn(p0, p1);
+                pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+              }
+              *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+            if (WM)
+              mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                           fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+            return (ls[0] + ls[1]) + (ls[2] + ls[3]);
+          };
+          auto own_max = [&]() -> float {
+            float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            if (lim >= KW - 1) {
+#pragma unroll
+              for (int e = 0; e < KW; e += 2)
+                mx4[(e >> 1) & 3] = fmax3(mx4[(e >> 1) & 3], __uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+            } else if (lim >= 0) {
+#pragma unroll
+              for (int e = 0; e < KW; ++e)
+                if (e <= lim) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(v[e]));
+            }
+            return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+          };
+          // joint raw max of the row: atomicMax on an order-preserving int
+          // image of the float into slot it % 3, one barrier over the row's
+          // NS warps; slot (it + 2) % 3 (last read before this barrier, next
+          // written after the following one) is reset here
+          auto exchange = [&](float mraw) -> float {
+            atomicMax(&s_cmx[it % 3][r], ord_f32(mraw));
+            switch (quarter) {                  // literal ids: a register id reserves all 16 barriers
+              case 0: asm volatile("bar.sync 2, %0;" ::"n"(NS * 32) : "memory"); break;
+              case 1: asm volatile("bar.sync 3, %0;" ::"n"(NS * 32) : "memory"); break;
+              case 2: asm volatile("bar.sync 4, %0;" ::"n"(NS * 32) : "memory"); break;
+              default: asm volatile("bar.sync 5, %0;" ::"n"(NS * 32) : "memory"); break;
+            }
+            const float m = a.sl2 * unord_f32(s_cmx[it % 3][r]);
+            if (hq == 0) s_cmx[(it + 2) % 3][r] = ORD_NEG_INF;
+            return m;
+          };
+          // m moves: rescale O (after P_{it-1} V_{it-1}) and the running sum
+          auto move_m = [&](float m_row) {
+            const bool move = m_row > m_use + RESCALE || (m_use == -INFINITY && m_row > -INFINITY);
+            const float sc = (move && m_use != -INFINITY) ? exp2f(m_use - m_row) : 1.f;
+            const bool resc = move && m_use != -INFINITY && it > 0;
+            if (move) {
+              l_run *= m_use == -INFINITY ? 0.f : sc;
+              m_use = m_row;
+            }
+            if (__any_sync(0xffffffffu, resc)) {
+              lp::mbar_wait(&o_done, (it - 1) & 1);
+              fence_after();
+              uint32_t o[HH];
+#pragma unroll
+              for (int cg = 0; cg < HH / 32; ++cg)
+                ld32(trow + C::O_COL + hq * HH + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(o + cg * 32));
+              wait_ld();
+#pragma unroll
+              for (int e = 0; e < HH; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * sc);
+#pragma unroll
+              for (int cg = 0; cg < HH / 32; ++cg)
+                st32(trow + C::O_COL + hq * HH + cg * 32, *reinterpret_cast<uint32_t(*)[32]>(o + cg * 32));
+              wait_st();
+            }
+            return move;
+          };
+          float ls, mraw = -INFINITY;
+          if (__any_sync(0xffffffffu, m_use == -INFINITY && lim >= 0)) {
+            // a row of the warp has no m yet: max first, then P
+            const float m_row = exchange(own_max());
+            if (warp == 2 && lane == 0) TRACE(6, it);
+            move_m(m_row);
+            ls = write_p(m_use, mraw, std::false_type{});
+          } else {
+            ls = write_p(m_use, mraw, std::true_type{});
+            if (warp == 2 && lane == 0) TRACE(6, it);
+            const bool moved = move_m(exchange(mraw));
+            if (__any_sync(0xffffffffu, moved)) {      // write_p is warp-collective; rewrites are idempotent
+              const float ls_new = write_p(m_use, mraw, std::false_type{});
+              if (moved) ls = ls_new;
+            }
+          }
+          l_run += ls;
+          fence_before();
+          if (warp == 2 && lane == 0) TRACE(4, it);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[b]);
+          if (warp == 2 && lane == 0) TRACE(5, it);
+          continue;
+        }
         const int lim = mine ? prow - c * TC_KEYS - h * 64 : -1;   // my keys 0..lim are visible
         const int limp = mine ? prow - c * TC_KEYS - (h ^ 1) * 64 : -1;   // the partner half's
         // the row max over all 128 keys: own half kept in registers, the
@@ -402,14 +642,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (warp == 2 && lane == 0) TRACE(5, it);
       }
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    s_mx[h][r] = l_run;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const float l_tot = l_run + s_mx[h ^ 1][r];
     if (it > 0) {
-      lp::mbar_wait(&o_done, (it - 1) & 1);          // the last P V has landed
+      lp::mbar_wait(&o_final, 0);                    // the last P V has landed
       fence_after();
     }
+    // row sums across the NS warps through the P buffers (free once the
+    // last P V has landed), summed in a fixed order
+    float* lsum = reinterpret_cast<float*>(sm + C::OFF_P);
+    lsum[hq * TC_M + r] = l_run;
+    asm volatile("bar.sync 1, %0;" ::"n"(NS * 128) : "memory");
+    float l_tot = 0.f;
+#pragma unroll
+    for (int j = 0; j < NS; ++j) l_tot += lsum[j * TC_M + r];
     uint32_t o[HH];
 #pragma unroll
     for (int cg = 0; cg < HH / 32; ++cg)
@@ -460,7 +704,8 @@ struct PpCfg {
   static constexpr int OFF_K = 2 * Q_BYTES;              // 2 stages
   static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;     // 2 stages
   static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;     // [tile][2]
-  static constexpr int SMEM = OFF_P + 4 * P_BYTES + 1024;
+  static constexpr int BODY = OFF_P + 4 * P_BYTES;
+  static constexpr int SMEM = BODY + 1024;
   static constexpr int TILE_COLS = 256;                  // per tile: S0 [0,64), S1 [64,128), O [128, 128 + HD)
 };
 
@@ -471,8 +716,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   using C = PpCfg<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  if (threadIdx.x == 0) {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if ((uint32_t)(sm - smem_raw) + C::BODY > dyn) __trap();   // launch_tc's pad assumption broken
+  }
   __shared__ __align__(8) uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2][2], s_empty[2][2],
-      p_full[2][2], o_done[2];
+      p_full[2][2], o_done[2], o_final;
   __shared__ uint32_t tmem_base;
   __shared__ int s_pos[2 * TC_M];
   __shared__ int16_t s_seq[2 * TC_M];
@@ -496,6 +746,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       }
       lp::mbar_init(&o_done[b], 1);
     }
+    lp::mbar_init(&o_final, 1);
     lp::fence_mbar_init();
   }
   if (warp == 1) {
@@ -606,6 +857,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       if (total > 0) {
         issue_pv(0, total - 1);
         issue_pv(1, total - 1);
+        commit(&o_final);
       }
     }
   } else if (warp <= 9) {
@@ -706,7 +958,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       }
     }
     if (it > 0) {
-      lp::mbar_wait(&o_done[t], (it - 1) & 1);
+      lp::mbar_wait(&o_final, 0);
       fence_after();
     }
     const bool live = i < nvalid && l_run > 0.f;
@@ -768,15 +1020,20 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   using C = TcCfg<HD>;
   const int G = H / KV;
   const int R = TC_M / G;
-  // LP_ATTN_TC: 1 = one Q tile per CTA (default), 2 = the ping-pong variant.
-  // Measured (profiles/r02/attn_prefill_pingpong_ab.txt): ping-pong wins on
-  // many short prompts (8 x 512 rows: 84 -> 70 us 8B, 143 -> 109 us 70B) and
-  // loses on one long one (1 x 2048: 83 -> 94 us, half as many, twice as long
-  // CTAs on 148 SMs); its two softmax warpgroups stay in phase, so the SFU /
-  // MMA overlap it was built for does not materialise yet.
+  // LP_ATTN_TC selects the variant (A/B tables: profiles/r02/attn_prefill_*):
+  //   3 (default) one Q tile per CTA, lazy row max (exchanged after the exp
+  //     pass; P recomputed only when m moves), packed FFMA2/FADD2/FMNMX3 math
+  //     and one key pair in four on the FMA-pipe exp2: 1 x 2048 rows 82.7 ->
+  //     80.2 us (8B), 2 x 4096 rows 439 -> 418 us (8B), 847 -> 804 us (70B);
+  //   1 the eager one-tile kernel (row max first, partner half streamed);
+  //   4 variant 3 with four warps per row quarter (32 keys each; slower);
+  //   5 / 6 variant 3 with no / half the exponentials on the FMA pipe;
+  //   2 the ping-pong kernel: wins on many short prompts (8 x 512 rows: 84 ->
+  //     72 us 8B, 144 -> 115 us 70B), loses on long ones (half as many, twice
+  //     as long CTAs on 148 SMs).
   static const int variant = [] {
     const char* e = getenv("LP_ATTN_TC");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 3;
   }();
   const uint32_t kbox = variant == 2 ? PP_KEYS : TC_KEYS;
   CUtensorMap mq, mk, mv;
@@ -791,8 +1048,23 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   static uint64_t attr = 0;
   int dev = 0;
   LP_CUDA(cudaGetDevice(&dev));
+  // dynamic bytes per instantiation: body + 1024-B alignment pad after the static smem
+  auto smem_for = [](auto kern) -> int {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return -1;
+    const int bytes = C::BODY + (int)((1024 - fa.sharedSizeBytes % 1024) % 1024);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return -1;
+    return bytes;
+  };
+  static int tc_smem[5] = {0, 0, 0, 0, 0};
   if (!(attr >> dev & 1)) {
-    LP_CUDA(cudaFuncSetAttribute(attention_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    tc_smem[0] = smem_for(attention_tc_kernel<HD, 2, false>);
+    tc_smem[1] = smem_for(attention_tc_kernel<HD, 2, true>);
+    tc_smem[2] = HD == 128 ? smem_for(attention_tc_kernel<128, 4, true>) : 0;
+    tc_smem[3] = smem_for(attention_tc_kernel<HD, 2, true, 0>);
+    tc_smem[4] = smem_for(attention_tc_kernel<HD, 2, true, 2>);
+    LP_CHECK(tc_smem[0] > 0 && tc_smem[1] > 0 && tc_smem[2] >= 0, "attention_tc: smem attributes: %s",
+             cudaGetErrorString(cudaGetLastError()));
     attr |= 1ull << dev;
   }
   static long long* trace = [] {     // device memory: a managed buffer's page faults distort the stamps
@@ -828,7 +1100,16 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     return 0;
   }
   const dim3 grid((unsigned)((T + R - 1) / R), (unsigned)KV);
-  LP_CUDA(lp::launch(attention_tc_kernel<HD>, grid, dim3(TC_THREADS), C::SMEM, s, mq, mk, mv, args));
+  if (variant == 4 && HD == 128)
+    LP_CUDA(lp::launch(attention_tc_kernel<128, 4, true>, grid, dim3(19 * 32), tc_smem[2], s, mq, mk, mv, args));
+  else if (variant == 5)      // lazy, SFU only
+    LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, true, 0>, grid, dim3(11 * 32), tc_smem[3], s, mq, mk, mv, args));
+  else if (variant == 6)      // lazy, half the exponentials on the FMA pipe
+    LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, true, 2>, grid, dim3(11 * 32), tc_smem[4], s, mq, mk, mv, args));
+  else if (variant == 1)
+    LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, false>, grid, dim3(11 * 32), tc_smem[0], s, mq, mk, mv, args));
+  else
+    LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, true>, grid, dim3(11 * 32), tc_smem[1], s, mq, mk, mv, args));
   if (trace) {
     static long long h[64 * 16];
     LP_CUDA(cudaStreamSynchronize(s));
