@@ -45,6 +45,7 @@ struct GemmArgs {
   int kb_per_split;   // k blocks per z-split
   int atomic;         // EPI_ADD with split-K: red.add; without: plain read-modify-write
   int tiles_n, tiles_t, splits;   // persistent kernel tile space
+  int streamk;        // CTA-pair kernel: equal k-block spans per cluster (EPI_ADD only, splits = 1)
 };
 
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
@@ -590,14 +591,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     nkb = min(args.k_blocks, kb0 + args.kb_per_split) - kb0;
   };
 
+  // work items of this cluster.  Default: whole tiles (x K splits) dealt
+  // round-robin.  Stream-K tail (args.streamk; accumulating epilogue only):
+  // the full waves stay round-robin (neighbouring clusters share operand
+  // tiles in L2), and only the k-blocks of the last partial wave's tiles are
+  // laid end to end and cut into nclusters equal spans (QKV T = 4096: 384
+  // pair tiles = 5 waves of 74 + 14 tiles, i.e. 12 k-blocks per cluster
+  // instead of a sixth round); a tile cut between clusters is summed by the
+  // red.add epilogue.  Positions p are k-block indices (tile * KB + kb).
+  const int64_t KB = args.k_blocks;
+  const int full = args.streamk ? (total / nclusters) * nclusters : total;
+  const int64_t p_full = (int64_t)full * KB;
+  const int64_t w_tail = (int64_t)(total - full) * KB;
+  const int64_t sk_beg = p_full + w_tail * cid / nclusters, sk_end = p_full + w_tail * (cid + 1) / nclusters;
+  const int64_t p_first = !args.streamk ? (int64_t)cid : (cid < full ? (int64_t)cid * KB : sk_beg);
+  auto valid = [&](int64_t p) { return args.streamk ? p < sk_end : p < (int64_t)total; };
+  auto decode = [&](int64_t p, int& n0, int& t0, int& kb0, int& nkb) {
+    if (args.streamk) {
+      int d0, d1;
+      tile_coords((int)(p / KB), n0, t0, d0, d1);
+      kb0 = (int)(p % KB);
+      nkb = p < p_full ? (int)KB : (int)min((int64_t)(KB - kb0), sk_end - p);
+    } else {
+      tile_coords((int)p, n0, t0, kb0, nkb);
+    }
+  };
+  auto advance = [&](int64_t p, int nkb) -> int64_t {
+    if (!args.streamk) return p + nclusters;
+    if (p < p_full) {
+      const int64_t q = p + (int64_t)nclusters * KB;
+      return q < p_full ? q : sk_beg;
+    }
+    return p + nkb;
+  };
+
   if (threadIdx.x == 0) lp::pdl_trigger();
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs) ----------------
     lp::pdl_wait();
     int it = 0;
-    for (int tile = cid; tile < total; tile += nclusters) {
+    for (int64_t p = p_first; valid(p);) {
       int n0, t0, kb0, nkb;
-      tile_coords(tile, n0, t0, kb0, nkb);
+      decode(p, n0, t0, kb0, nkb);
+      p = advance(p, nkb);
       for (int i = 0; i < nkb; ++i, ++it) {
         const int s = it % C::STAGES;
         lp::mbar_wait(&empty_bar[s], ((it / C::STAGES) & 1) ^ 1);
@@ -614,9 +650,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     // ---------------- MMA issuer (leader CTA only) ----------------
     constexpr uint32_t idesc = idesc2_bf16_f32<BT>();
     int it = 0, li = 0;
-    for (int tile = cid; tile < total; tile += nclusters, ++li) {
+    for (int64_t p = p_first; valid(p); ++li) {
       int n0, t0, kb0, nkb;
-      tile_coords(tile, n0, t0, kb0, nkb);
+      decode(p, n0, t0, kb0, nkb);
+      p = advance(p, nkb);
       const int a = li % C::NBUF;
       mbar_wait_cluster(&tempty[a], ((li / C::NBUF) & 1) ^ 1);   // both CTAs drained this accumulator
       tc_fence_after();
@@ -647,9 +684,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     const uint32_t leader_tempty0 = mapa_rank(lp::smem_u32(&tempty[0]), 0);
     const uint32_t leader_tempty1 = mapa_rank(lp::smem_u32(&tempty[1]), 0);
     int li = 0;
-    for (int tile = cid; tile < total; tile += nclusters, ++li) {
+    for (int64_t p = p_first; valid(p); ++li) {
       int n0, t0, kb0, nkb;
-      tile_coords(tile, n0, t0, kb0, nkb);
+      decode(p, n0, t0, kb0, nkb);
+      p = advance(p, nkb);
       const int a = li % C::NBUF;
       lp::mbar_wait(&tfull[a], (li / C::NBUF) & 1);
       tc_fence_after();
@@ -804,6 +842,7 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
   a.tiles_n = (int)((N + BM - 1) / BM);
   a.tiles_t = (int)((T + BT - 1) / BT);
   a.splits = splits;
+  a.streamk = 0;
   if constexpr (BT >= 32) {
     if (pair) {
       CUtensorMap mxh;
@@ -811,7 +850,20 @@ int launch(const void* W, const void* W2, int64_t N, int64_t K, const void* X, i
       static int sms2 = 0;
       if (!sms2) LP_CUDA(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev));
       const int total = ((a.tiles_n + 1) / 2) * a.tiles_t * a.splits;
-      const int clusters = total < sms2 / 2 ? total : sms2 / 2;
+      const int slots = sms2 / 2;
+      // stream-K tail for the accumulating epilogue when whole tiles leave a
+      // partial last wave (LP_GEMM_PAIR_STREAMK=0: round-robin tiles only);
+      // below one wave the caller's split-K policy balances instead
+      static int sk_env = -1;
+      if (sk_env < 0) {
+        const char* e = getenv("LP_GEMM_PAIR_STREAMK");
+        sk_env = (e && e[0] == '0') ? 0 : 1;
+      }
+      // (a tail above 80 % of a wave measured faster as a plain last round:
+      // 70B down T = 4096, 68 of 74 slots: 1332 vs 1407 us)
+      a.streamk = (EPI == EPI_ADD_F32 && sk_env && a.splits == 1 && total > slots && total % slots != 0 &&
+                   (total % slots) * 10 <= 8 * slots) ? 1 : 0;
+      const int clusters = total < slots ? total : slots;
       LP_CUDA(lp::launch(gemm_pair_kernel<BT, EPI>, dim3(2 * clusters), dim3(PAIR_THREADS), Cfg2<BT, EPI>::SMEM, s, mw,
                          mw2, mxh, a));
       return 0;

@@ -31,10 +31,6 @@ from . import _native as N
 from .engine import device_view
 from .image import ImageLayout
 
-_SMS = 148
-GEMM_PAIR = os.environ.get("LP_GEMM_PAIR", "1") != "0"   # mirrors lp_gemm.cu's switch
-
-
 def _vp(x):
     return C.c_void_p(x if isinstance(x, int) else x.data_ptr())
 
@@ -49,7 +45,8 @@ def _cur_stream(stream):
 
 
 SMS = 148
-GEMM_PAIR = os.environ.get("LP_GEMM_PAIR", "1") != "0"   # mirrors lp_gemm.cu's switch
+GEMM_PAIR = os.environ.get("LP_GEMM_PAIR", "1") != "0"   # mirrors lp_gemm.cu's switches
+GEMM_PAIR_STREAMK = os.environ.get("LP_GEMM_PAIR_STREAMK", "1") != "0"
 
 
 def gemm_token_tile(tokens: int) -> int:
@@ -78,6 +75,10 @@ def gemm_split(n_rows: int, k: int, tokens: int) -> int:
     slots = SMS // 2 if GEMM_PAIR else SMS
     rows = 256 if GEMM_PAIR else 128
     tiles = -(-n_rows // rows) * -(-tokens // gemm_token_tile(tokens))
+    if GEMM_PAIR and GEMM_PAIR_STREAMK and tiles > slots and (tiles % slots) * 10 <= 8 * slots:
+        # more than one wave: the kernel's stream-K tail balances the last
+        # partial wave itself (same condition as lp_gemm.cu; profiles/r02/gemm_streamk_ab.txt)
+        return 1
     if tiles >= 2 * slots:
         # >= 2 waves: tiles finish at staggered times, so quantisation costs
         # less than modelled, while shorter K per item exposes the red.add

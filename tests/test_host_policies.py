@@ -54,11 +54,18 @@ def test_admission_respects_capacity_and_inactive_units():
         assert r.unit == 0 and r.needs_prefill and r.kv_len == 0
 
 
-def test_gemm_split_policy():
+def test_gemm_split_policy(monkeypatch):
     # decode: ~160 CTAs of one wave (profiles/gemm_split_sweep_r01.txt), >= 4 k-blocks per split
     assert L.gemm_split(6144, 4096, 16) == 3
     assert L.gemm_split(4096, 14336, 1) == 5
     assert L.gemm_split(32000, 256, 8) == 1
+    # prefill beyond one wave of pair tiles with the kernel's stream-K tail
+    # (default): no split (WO T = 2048: 128 tiles for 74 slots)
+    assert L.GEMM_PAIR_STREAMK
+    for n, k, t in ((4096, 4096, 2048), (4096, 14336, 4096), (10240, 8192, 1024)):
+        assert L.gemm_split(n, k, t) == 1
+    assert L.gemm_split(6144, 4096, 256) == 3      # below one wave: split-K as before
+    monkeypatch.setattr(L, "GEMM_PAIR_STREAMK", False)   # LP_GEMM_PAIR_STREAMK=0: wave-efficiency split
     # prefill: QKV at T = 256 has 24 pair tiles for 74 cluster slots -> split
     assert L.gemm_split(6144, 4096, 256) == 3
     # >= 2 waves of tiles: never split (T = 4096, 8B shapes)

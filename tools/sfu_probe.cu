@@ -4,6 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/sfu tools/sfu_probe.cu && /tmp/sfu
 #include <cstdio>
 #include <cstdint>
+#include <cuda_fp16.h>
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -33,7 +34,15 @@ __global__ void k(float* out, long long* clk, int iters) {
     for (int j = 0; j < 8; ++j) {
       if (MODE == 0) a[j] = ex2(a[j]) - 1.0f;
       else if (MODE == 1) a[j] = ex2_poly(a[j]) - 1.0f;
-      else a[j] = (j & 1 ? ex2_poly(a[j]) : ex2(a[j])) - 1.0f;
+      else if (MODE == 2) a[j] = (j & 1 ? ex2_poly(a[j]) : ex2(a[j])) - 1.0f;
+      else if (MODE == 3) {       // F2FP pack (fp32 pair -> half2) + unpack-free feedback
+        const __half2 h = __floats2half2_rn(a[j], a[j ^ 1]);
+        a[j] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&h)) * 1e-30f - 0.5f;
+      } else {                    // MUFU.EX2 then F2FP (the softmax's per-pair work)
+        const float e0 = ex2(a[j]);
+        const __half2 h = __floats2half2_rn(e0, e0);
+        a[j] = __uint_as_float(*reinterpret_cast<const uint32_t*>(&h)) * 1e-30f - 0.5f;
+      }
     }
   }
   __syncthreads();
@@ -52,17 +61,18 @@ int main() {
   cudaMalloc(&out, sms * 1024 * 4);
   cudaMalloc(&clk, sms * 8);
   const int iters = 4096;
-  const char* names[3] = {"MUFU.EX2", "FMA poly exp2", "half MUFU / half poly"};
-  for (int mode = 0; mode < 3; ++mode)
+  const char* names[5] = {"MUFU.EX2", "FMA poly exp2", "half MUFU / half poly", "F2FP pack (+FMUL/FADD)",
+                          "MUFU.EX2 + F2FP"};
+  for (int mode = 0; mode < 5; ++mode)
     for (int warps : {4, 8, 16, 32}) {
-      auto fn = mode == 0 ? k<0> : mode == 1 ? k<1> : k<2>;
+      auto fn = mode == 0 ? k<0> : mode == 1 ? k<1> : mode == 2 ? k<2> : mode == 3 ? k<3> : k<4>;
       fn<<<sms, warps * 32>>>(out, clk, iters);
       fn<<<sms, warps * 32>>>(out, clk, iters);
       cudaDeviceSynchronize();
       long long c;
       cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
       const double ops = (double)warps * 32 * 8 * iters;
-      printf("%-24s warps/SM %2d: %.2f exp2 per clock per SM\n", names[mode], warps, ops / c);
+      printf("%-24s warps/SM %2d: %.2f ops per clock per SM\n", names[mode], warps, ops / c);
     }
   return 0;
 }
