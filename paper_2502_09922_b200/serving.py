@@ -105,9 +105,11 @@ class Unit:
 class Server:
     """Serves a request trace while ``plan`` is being multicast."""
 
+    PREFILL_PASS_FLOP = 8.2e12     # pipeline prefill budget per pass (see __init__)
+
     def __init__(self, plan, cluster, local_slots: int = 8, max_len: int = 512, switch_hold_tokens: int = 0,
                  prefill_ms_per_token: float = 0.5, use_graphs: bool = True, pipeline_batch: int = 1,
-                 pipeline_prefill_tokens: int = 512):
+                 pipeline_prefill_tokens: int | None = None):
         """``pipeline_batch``: requests per pipeline slot.  The reference's
         capacity is one request per stage (pipeline.py:43-46) — with its
         one-request local units (``batch_slots = 1``, simengine.py:236).
@@ -118,9 +120,10 @@ class Server:
 
         ``pipeline_prefill_tokens``: prompt tokens a pipeline pass prefills
         (at least one request; the rest keep waiting in their slots, decodes
-        always run).  Without it a burst admitted into a wide pipeline is one
-        long prefill that pushes every first token past the first full
-        replica."""
+        always run).  Default: ~8 TFLOP of prompt per pass (PREFILL_PASS_FLOP),
+        512 tokens for Llama-3-8B and one request for 70B.  Without a budget
+        a burst admitted into a wide pipeline is one long prefill that pushes
+        every first token past the first full replica."""
         import torch
         self.plan = plan
         self.cluster = cluster
@@ -132,6 +135,8 @@ class Server:
         self.use_graphs = use_graphs
         self.prefill_ms_per_token = prefill_ms_per_token
         self.pipeline_batch = max(1, int(pipeline_batch))
+        if pipeline_prefill_tokens is None:
+            pipeline_prefill_tokens = self.PREFILL_PASS_FLOP / (2.0 * plan.layout.weights_bytes / 2)
         self.pipeline_prefill_tokens = max(1, int(pipeline_prefill_tokens))
         self.events = []
         self.profile = []          # per iteration: (start, enqueue s, device s, tokens, unit batches)

@@ -21,7 +21,7 @@ def run_serving(n_gpus: int, model: str = "llama3-8b", k: int = 2, blocks: int =
                 prompt_len: int = 128, out_tokens: int = 32, spacing_s: float = 0.001, pull_ctas: int = 32,
                 local_slots: int = 16, seed: int = 20250815, executor: str = "ce", outdir: str | None = None,
                 node_devices: list | None = None, host_source: bool = False, pipeline_batch: int | None = None,
-                pipeline_prefill_tokens: int = 512):
+                pipeline_prefill_tokens: int | None = None):
     """host_source: the tier-driven plan (scaleout.plan_from_tiers) with GPU 0
     holding the model and the box's pinned host copy as the second source
     (k = 2): one sub-group is fed over PCIe, GPUs 1..n-1 are cold."""
@@ -131,8 +131,8 @@ if __name__ == "__main__":
     ap.add_argument("--host-source", action="store_true", help="GPU 0 + the pinned host copy as the k = 2 sources")
     ap.add_argument("--pipeline-batch", type=int, default=None,
                     help="requests per pipeline slot (default = local slots; 1 = the reference's capacity)")
-    ap.add_argument("--pipeline-prefill-tokens", type=int, default=512,
-                    help="prompt tokens one pipeline pass prefills (serving.Server)")
+    ap.add_argument("--pipeline-prefill-tokens", type=int, default=None,
+                    help="prompt tokens one pipeline pass prefills (default: serving.Server's FLOP budget)")
     a = ap.parse_args()
     print(json.dumps(run_serving(a.gpus, a.model, a.k, a.blocks, a.requests, out_tokens=a.out_tokens,
                                  executor=a.executor, pull_ctas=a.pull_ctas, outdir=a.outdir,
