@@ -38,7 +38,10 @@ def _ptr(t):
 @pytest.mark.parametrize("n,k,t,epi,split", [
     (128, 64, 16, 1, 1), (256, 256, 1, 1, 1), (300, 688, 5, 1, 1), (1024, 1024, 33, 0, 4),
     (4096, 512, 100, 0, 2), (384, 4096, 300, 1, 1), (640, 1536, 256, 0, 1), (32000, 256, 24, 1, 1),
-    (512, 4096, 7, 0, 8)])
+    (512, 4096, 7, 0, 8),
+    # CTA-pair stream-K tail (> 1 wave of 74 pair tiles, tail <= 80 %): 192 tiles, 8 k-blocks each;
+    # 160 ragged tiles whose tail spans are 1-2 k-blocks
+    (6144, 512, 2048, 0, 1), (5000, 640, 1900, 0, 1)])
 def test_gemm_matches_fp32(n, k, t, epi, split):
     import torch
     g = torch.Generator(device="cuda").manual_seed(n * 7 + k)
