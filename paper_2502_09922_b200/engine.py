@@ -279,11 +279,14 @@ def _fit_ctas(device: int, n_exec: int, push_ctas: int, pull_ctas: int) -> tuple
     per = push_ctas + pull_ctas
     if n_exec * per <= sms:
         return push_ctas, pull_ctas
-    room = max(1, sms // max(1, n_exec))
-    push = (push_ctas * room) // per if push_ctas else 0
+    room = sms // max(1, n_exec)
+    if room < (push_ctas > 0) + (pull_ctas > 0):
+        raise ValueError(f"{n_exec} nodes on device {device} leave {room} CTAs each: too few for the "
+                         f"push and pull roles")
+    push = max(1, (push_ctas * room) // per) if push_ctas else 0
     pull = room - push if pull_ctas else 0
-    if push_ctas and push == 0:
-        push, pull = 1, max(0, room - 1) if pull_ctas else 0
+    if pull_ctas and pull < 1:
+        push, pull = push - 1, 1
     return push, pull
 
 

@@ -76,3 +76,21 @@ def test_gemm_split_policy(monkeypatch):
         s = L.gemm_split(n, k, t)
         assert s == 1 or (k // 64) // s >= 8
     assert L.gemm_token_tile(1) == 16 and L.gemm_token_tile(65) == 128 and L.gemm_token_tile(129) == 256
+
+
+def test_fit_ctas_shares_one_device(monkeypatch):
+    """Several schedule nodes on one device (tests, host-fed boxes): the
+    per-node CTA counts shrink so every CTA of the dataflow is co-resident."""
+    import torch
+    from paper_2502_09922_b200 import engine as E
+
+    class Props:
+        multi_processor_count = 148
+    monkeypatch.setattr(torch.cuda, "get_device_properties", lambda d: Props())
+    assert E._fit_ctas(0, 4, 0, 32) == (0, 32)            # fits: unchanged
+    assert E._fit_ctas(0, 5, 0, 32) == (0, 29)            # 160 > 148
+    push, pull = E._fit_ctas(0, 5, 16, 16)
+    assert push >= 1 and pull >= 1 and 5 * (push + pull) <= 148
+    assert E._fit_ctas(0, 74, 1, 1) == (1, 1)
+    with pytest.raises(ValueError):
+        E._fit_ctas(0, 200, 0, 1)
