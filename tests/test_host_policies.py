@@ -9,6 +9,8 @@
 """
 from collections import deque
 
+import pytest
+
 from paper_2502_09922_b200 import llama as L
 from paper_2502_09922_b200.serving import Request, Server, Unit
 from paper_2502_09922_b200.workload import TraceRecord
