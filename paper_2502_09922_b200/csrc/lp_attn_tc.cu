@@ -184,6 +184,96 @@ __device__ __forceinline__ int ord_f32(float f) {
   return i >= 0 ? i : i ^ 0x7FFFFFFF;
 }
 __device__ __forceinline__ float unord_f32(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+// One thread's share of a softmax chunk: KW raw scores v (keys 0..lim of
+// them visible) -> fp16 P = exp2(v * sl2 - mu) into its 128-B swizzled smem
+// row (16-B chunks cb .. cb + KW / 8 - 1, XOR-swizzled by r & 7); returns the
+// row sum, and with WM the raw max over the visible keys in mraw.  Warp-
+// collective (the unmasked test is a vote).  Unmasked chunks use packed
+// FFMA2 / FADD2 / FMNMX3 and one key pair in four on the FMA-pipe exp2.
+template <int KW, bool WM, int POLY = 1>
+__device__ __forceinline__ float softmax_write_p(const uint32_t (&v)[KW], int lim, float sl2, float mu,
+                                                 uint8_t* prow_s, int cb, int r, float& mraw) {
+  const bool unmasked = __all_sync(0xffffffffu, lim >= KW - 1);   // before any lane returns
+  if (lim < 0) {
+#pragma unroll
+    for (int q = 0; q < KW / 8; ++q)
+      *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) = make_uint4(0, 0, 0, 0);
+    return 0.f;
+  }
+  const float nm = -mu;
+  if (unmasked) {
+    float2 ls2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    const float2 sl = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
+#pragma unroll
+    for (int q = 0; q < KW / 8; ++q) {
+      uint32_t pk[4];
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        const int k = q * 8 + e;
+        const float2 sv = make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1]));
+        if (WM) mx4[e >> 1] = fmax3(mx4[e >> 1], sv.x, sv.y);
+        const float2 x = ffma2(sv, sl, nm2);
+        float2 p;
+        if ((e >> 1) >= 4 - POLY) {      // POLY of every 4 key pairs on the FMA pipe
+          p = exp2_poly2(x);
+        } else {
+          p.x = fast_exp2(x.x);
+          p.y = fast_exp2(x.y);
+        }
+        ls2[e >> 1] = fadd2(ls2[e >> 1], p);
+        const __half2 hv = __floats2half2_rn(p.x, p.y);
+        pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+      }
+      *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+    if (WM) mraw = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+    const float2 s01 = fadd2(ls2[0], ls2[1]), s23 = fadd2(ls2[2], ls2[3]);
+    return (s01.x + s01.y) + (s23.x + s23.y);
+  }
+  float ls[4] = {0.f, 0.f, 0.f, 0.f};
+  float mx8[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < KW / 8; ++q) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const int k = q * 8 + e;
+      const float s0 = __uint_as_float(v[k]), s1 = __uint_as_float(v[k + 1]);
+      const float p0 = k <= lim ? fast_exp2(fmaf(s0, sl2, nm)) : 0.f;
+      const float p1 = k + 1 <= lim ? fast_exp2(fmaf(s1, sl2, nm)) : 0.f;
+      if (WM) {
+        mx8[e] = k <= lim ? fmaxf(mx8[e], s0) : mx8[e];
+        mx8[e + 1] = k + 1 <= lim ? fmaxf(mx8[e + 1], s1) : mx8[e + 1];
+      }
+      ls[e >> 1] += p0 + p1;
+      const __half2 hv = __floats2half2_rn(p0, p1);
+      pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  if (WM)
+    mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+  return (ls[0] + ls[1]) + (ls[2] + ls[3]);
+}
+// raw max over the visible keys 0..lim of v
+template <int KW>
+__device__ __forceinline__ float softmax_row_max(const uint32_t (&v)[KW], int lim) {
+  float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  if (lim >= KW - 1) {
+#pragma unroll
+    for (int e = 0; e < KW; e += 2)
+      mx4[(e >> 1) & 3] = fmax3(mx4[(e >> 1) & 3], __uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+  } else if (lim >= 0) {
+#pragma unroll
+    for (int e = 0; e < KW; ++e)
+      if (e <= lim) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(v[e]));
+  }
+  return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lp::smem_u32(bar)) : "memory");
 }
@@ -388,92 +478,10 @@ __global__ void __launch_bounds__((3 + 4 * NS) * 32, 1)
           if (warp == 2 && lane == 0) TRACE(3, it);
           uint8_t* prow_s = sm + C::OFF_P + b * C::P_BYTES + ((hq * KW) >> 6) * ATOM + (r >> 3) * 1024 + (r & 7) * 128;
           const int cb = ((hq * KW) & 63) >> 3;       // my first 16-B chunk of the 128-B P row
-          // P (fp16) of my keys into smem with m = mu; returns the row sum;
-          // with want_max also the raw max over the visible keys.  Unmasked
-          // chunks (the whole warp below the diagonal) take packed math and
-          // send one key pair in four through the FMA-pipe exp2.
           auto write_p = [&](float mu, float& mraw, auto want_max) -> float {
-            constexpr bool WM = decltype(want_max)::value;
-            const bool unmasked = __all_sync(0xffffffffu, lim >= KW - 1);   // before any lane returns
-            if (lim < 0) {
-#pragma unroll
-              for (int q = 0; q < KW / 8; ++q)
-                *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) = make_uint4(0, 0, 0, 0);
-              return 0.f;
-            }
-            const float nm = -mu;
-            if (unmasked) {
-              float2 ls2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-              float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-              const float2 sl = make_float2(a.sl2, a.sl2), nm2 = make_float2(nm, nm);
-#pragma unroll
-              for (int q = 0; q < KW / 8; ++q) {
-                uint32_t pk[4];
-#pragma unroll
-                for (int e = 0; e < 8; e += 2) {
-                  const int k = q * 8 + e;
-                  const float2 sv = make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1]));
-                  if (WM) mx4[e >> 1] = fmax3(mx4[e >> 1], sv.x, sv.y);
-                  const float2 x = ffma2(sv, sl, nm2);
-                  float2 p;
-                  if ((e >> 1) >= 4 - POLY) {      // POLY of every 4 key pairs on the FMA pipe
-                    p = exp2_poly2(x);
-                  } else {
-                    p.x = fast_exp2(x.x);
-                    p.y = fast_exp2(x.y);
-                  }
-                  ls2[e >> 1] = fadd2(ls2[e >> 1], p);
-                  const __half2 hv = __floats2half2_rn(p.x, p.y);
-                  pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
-                }
-                *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) =
-                    make_uint4(pk[0], pk[1], pk[2], pk[3]);
-              }
-              if (WM) mraw = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-              const float2 s01 = fadd2(ls2[0], ls2[1]), s23 = fadd2(ls2[2], ls2[3]);
-              return (s01.x + s01.y) + (s23.x + s23.y);
-            }
-            float ls[4] = {0.f, 0.f, 0.f, 0.f};
-            float mx8[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
-#pragma unroll
-            for (int q = 0; q < KW / 8; ++q) {
-              uint32_t pk[4];
-#pragma unroll
-              for (int e = 0; e < 8; e += 2) {
-                const int k = q * 8 + e;
-                const float s0 = __uint_as_float(v[k]), s1 = __uint_as_float(v[k + 1]);
-                float p0 = k <= lim ? fast_exp2(fmaf(s0, a.sl2, nm)) : 0.f;
-                float p1 = k + 1 <= lim ? fast_exp2(fmaf(s1, a.sl2, nm)) : 0.f;
-                if (WM) {
-                  mx8[e] = k <= lim ? fmaxf(mx8[e], s0) : mx8[e];
-                  mx8[e + 1] = k + 1 <= lim ? fmaxf(mx8[e + 1], s1) : mx8[e + 1];
-                }
-                ls[e >> 1] += p0 + p1;
-                const __half2 hv = __floats2half2_rn(p0, p1);
-                pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
-              }
-              *reinterpret_cast<uint4*>(prow_s + (((cb + q) ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            }
-            if (WM)
-              mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                           fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-            return (ls[0] + ls[1]) + (ls[2] + ls[3]);
+            return softmax_write_p<KW, decltype(want_max)::value, POLY>(v, lim, a.sl2, mu, prow_s, cb, r, mraw);
           };
-          auto own_max = [&]() -> float {
-            float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            if (lim >= KW - 1) {
-#pragma unroll
-              for (int e = 0; e < KW; e += 2)
-                mx4[(e >> 1) & 3] = fmax3(mx4[(e >> 1) & 3], __uint_as_float(v[e]), __uint_as_float(v[e + 1]));
-            } else if (lim >= 0) {
-#pragma unroll
-              for (int e = 0; e < KW; ++e)
-                if (e <= lim) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(v[e]));
-            }
-            return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-          };
+          auto own_max = [&]() -> float { return softmax_row_max<KW>(v, lim); };
           // joint raw max of the row: atomicMax on an order-preserving int
           // image of the float into slot it % 3, one barrier over the row's
           // NS warps; slot (it + 2) % 3 (last read before this barrier, next
@@ -842,23 +850,30 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         commit(&s_full[t][st]);
         if (t == 1) commit(&k_empty[st]);
       };
-      // ping-pong order: tile 1's S of chunk it waits for tile 0's P of the
-      // previous chunk, which keeps the two softmax warpgroups half a period
-      // apart (one in the SFU-heavy exp phase while the other loads / reduces)
+      // both tiles' S of chunk it + 1 go into the in-order tensor pipe before
+      // the P V of chunk it (S is double-buffered per tile): each softmax
+      // warpgroup finds its next S computed when it finishes a chunk, and the
+      // two warpgroups never wait on each other (an earlier order, S1(it)
+      // after P0(it - 1), chained them: ~2,870 cycles per chunk)
       lp::mbar_wait(&q_full, 0);
-      for (int it = 0; it < total; ++it) {
-        lp::mbar_wait(&k_full[it & 1], (it >> 1) & 1);
-        TRACE(0, it);
-        issue_s(0, it);
-        if (it > 0) issue_pv(0, it - 1);
-        issue_s(1, it);
-        if (it > 0) issue_pv(1, it - 1);
-      }
       if (total > 0) {
-        issue_pv(0, total - 1);
-        issue_pv(1, total - 1);
-        commit(&o_final);
+        lp::mbar_wait(&k_full[0], 0);
+        TRACE(0, 0);
+        issue_s(0, 0);
+        issue_s(1, 0);
       }
+      for (int it = 0; it < total; ++it) {
+        if (it + 1 < total) {
+          TRACE(10, it + 1);
+          lp::mbar_wait(&k_full[(it + 1) & 1], ((it + 1) >> 1) & 1);
+          TRACE(0, it + 1);
+          issue_s(0, it + 1);
+          issue_s(1, it + 1);
+        }
+        issue_pv(0, it);
+        issue_pv(1, it);
+      }
+      if (total > 0) commit(&o_final);
     }
   } else if (warp <= 9) {
     // ---------------- softmax: warpgroup t owns Q tile t, thread = row ----------------
@@ -888,68 +903,49 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[t][b]);
         if ((warp == 2 || warp == 6) && lane == 0) TRACE(3 + 4 * t, it);
-        float mx8[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = -INFINITY;
-        if (lim >= 63) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
-        } else if (lim >= 0) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e <= lim) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(v[e]));
-        }
-        const float m_row = a.sl2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        const bool move = m_row > m_use + RESCALE || (m_use == -INFINITY && m_row > -INFINITY);
-        const float sc = (move && m_use != -INFINITY) ? exp2f(m_use - m_row) : 1.f;
-        const bool resc = move && m_use != -INFINITY && it > 0;
-        if (move) {
-          l_run *= m_use == -INFINITY ? 0.f : sc;
-          m_use = m_row;
-        }
-        if (__any_sync(0xffffffffu, resc)) {           // rescale O in TMEM (warp-collective ld/st)
-          lp::mbar_wait(&o_done[t], (it - 1) & 1);
-          fence_after();
-#pragma unroll
-          for (int cg = 0; cg < HD / 32; ++cg) {
-            uint32_t o[32];
-            ld32(trow + 128 + cg * 32, o);
-            wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * sc);
-            st32(trow + 128 + cg * 32, o);
-          }
-          wait_st();
-        }
-        if ((warp == 2 || warp == 6) && lane == 0) TRACE(4 + 4 * t, it);
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        // lazy row max (one thread owns the row: no exchange): P with the
+        // current m and the raw max in one pass; only a move of m by more
+        // than RESCALE (first visible chunk, rare after) recomputes P
         uint8_t* prow_s = sm + C::OFF_P + (t * 2 + b) * C::P_BYTES + (r >> 3) * 1024 + (r & 7) * 128;
-        if (lim < 0) {
+        auto move_m = [&](float m_row) {
+          const bool move = m_row > m_use + RESCALE || (m_use == -INFINITY && m_row > -INFINITY);
+          const float sc = (move && m_use != -INFINITY) ? exp2f(m_use - m_row) : 1.f;
+          const bool resc = move && m_use != -INFINITY && it > 0;
+          if (move) {
+            l_run *= m_use == -INFINITY ? 0.f : sc;
+            m_use = m_row;
+          }
+          if (__any_sync(0xffffffffu, resc)) {         // rescale O in TMEM (warp-collective ld/st)
+            lp::mbar_wait(&o_done[t], (it - 1) & 1);   // P V of chunk it - 1 has landed
+            fence_after();
 #pragma unroll
-          for (int q = 0; q < 8; ++q) *reinterpret_cast<uint4*>(prow_s + q * 16) = make_uint4(0, 0, 0, 0);
-        } else {
-          const float nm = -m_use;
+            for (int cg = 0; cg < HD / 32; ++cg) {
+              uint32_t o[32];
+              ld32(trow + 128 + cg * 32, o);
+              wait_ld();
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-              const int k = q * 8 + e;
-              float p0 = fast_exp2(fmaf(__uint_as_float(v[k]), a.sl2, nm));
-              float p1 = fast_exp2(fmaf(__uint_as_float(v[k + 1]), a.sl2, nm));
-              if (lim < 63) {
-                p0 = k <= lim ? p0 : 0.f;
-                p1 = k + 1 <= lim ? p1 : 0.f;
-              }
-              ls[e >> 1] += p0 + p1;
-              const __half2 hv = __floats2half2_rn(p0, p1);
-              pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * sc);
+              st32(trow + 128 + cg * 32, o);
             }
-            *reinterpret_cast<uint4*>(prow_s + ((q ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            wait_st();
+          }
+          return move;
+        };
+        float ls, mraw = -INFINITY;
+        if (__any_sync(0xffffffffu, m_use == -INFINITY && lim >= 0)) {
+          move_m(a.sl2 * softmax_row_max<PP_KEYS>(v, lim));
+          if ((warp == 2 || warp == 6) && lane == 0) TRACE(4 + 4 * t, it);
+          ls = softmax_write_p<PP_KEYS, false>(v, lim, a.sl2, m_use, prow_s, 0, r, mraw);
+        } else {
+          ls = softmax_write_p<PP_KEYS, true>(v, lim, a.sl2, m_use, prow_s, 0, r, mraw);
+          if ((warp == 2 || warp == 6) && lane == 0) TRACE(4 + 4 * t, it);
+          const bool moved = move_m(a.sl2 * mraw);
+          if (__any_sync(0xffffffffu, moved)) {        // warp-collective rewrite, idempotent where m stayed
+            const float ls_new = softmax_write_p<PP_KEYS, false>(v, lim, a.sl2, m_use, prow_s, 0, r, mraw);
+            if (moved) ls = ls_new;
           }
         }
-        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        l_run += ls;
         fence_before();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -1092,9 +1088,9 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
       LP_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
       for (int it = 0; it < 64 && h[it * 16]; ++it) {
         const long long* t = h + it * 16;
-        fprintf(stderr, "pp chunk %2d: K_ready %7lld | tile0 S_ready %7lld ld %+5lld max %+5lld P %+5lld | tile1 S_ready "
-                "%7lld ld %+5lld max %+5lld P %+5lld\n", it, t[0] - h[0], t[2] - h[0], t[3] - t[2], t[4] - t[3],
-                t[5] - t[4], t[6] - h[0], t[7] - t[6], t[8] - t[7], t[9] - t[8]);
+        fprintf(stderr, "pp chunk %2d: mma_at %7lld K_ready %7lld | tile0 S_ready %7lld ld %+5lld exp %+5lld P %+5lld | "
+                "tile1 S_ready %7lld ld %+5lld exp %+5lld P %+5lld\n", it, t[10] ? t[10] - h[0] : 0, t[0] - h[0],
+                t[2] - h[0], t[3] - t[2], t[4] - t[3], t[5] - t[4], t[6] - h[0], t[7] - t[6], t[8] - t[7], t[9] - t[8]);
       }
     }
     return 0;
