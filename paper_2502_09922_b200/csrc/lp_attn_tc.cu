@@ -1,6 +1,12 @@
 // Causal GQA prefill attention on the 5th-gen tensor cores (tcgen05 + TMEM +
 // TMA), FlashAttention-style online softmax.
 //
+// Default: attention_fa_kernel (FA4 layout, below the one-tile kernel): two
+// Q tiles per CTA, P kept in TMEM as the P V MMA's A operand, one softmax
+// thread per row.  The one-tile kernel described first stays selectable
+// (LP_ATTN_TC=1/3, launch_tc) and shares the tiling, TMA boxes and the
+// MN-major V operand.
+//
 // Tile: one CTA owns 128 TMEM lanes = R tokens x G query heads of one kv head
 // (R = 128 / G; Llama-3-8B G = 4 -> 32 tokens, 70B G = 8 -> 16, MHA -> 128),
 // so the heads of a GQA group share every K/V chunk the CTA streams.  Rows
@@ -116,6 +122,19 @@ __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait for outstanding tcgen05.ld with v's registers as in-out operands: the
+// compiler cannot read, move or reuse them before the loads have landed
+// (needed when a load stays in flight across other code)
+__device__ __forceinline__ void wait_ld32(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                 "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -1010,6 +1029,357 @@ int map3d(CUtensorMap* m, CUtensorMapDataType ty, const void* base, uint64_t d0,
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// FA4-layout variant (LP_ATTN_TC=7): two Q tiles per CTA over 128-key chunks
+// with P kept in TMEM.  Tile t owns TMEM columns [256 t, 256 t + 256): S_t at
+// [0, 128) (fp32), O_t at [128, 128 + HD); P_t (fp16 pairs) overwrites S_t's
+// first 64 columns once the softmax has read them, and O_t += P_t V is a
+// tcgen05.mma with the A operand read from TMEM (row = lane, 16 keys = 8
+// columns per k-step; layout validated by tools/umma_ts_probe.cu), so the
+// P V MMA moves only V through smem.  Smem: Q 2 x 32 KB + K / V rings 2 x 2 x
+// 32 KB.  Per tile the chain is S_t(j) -> softmax_t(j) -> P_t(j) V -> S_t(j+1)
+// (single S buffer: the in-order tensor pipe issues S_t(j+1) after the P V
+// that reads P_t(j) from the same columns), and the other tile's MMAs run
+// under each softmax.  Softmax: one thread per row, a max pass and an exp
+// pass over the S columns (no exchange, no recompute); O is rescaled in TMEM
+// without waiting (S_t(j) complete implies P_t(j-1) V complete).
+constexpr int FA_THREADS = 352;   // warp 0 TMA Q + K, 1 MMA, 2-5 softmax tile 0, 6-9 tile 1, 10 TMA V
+
+template <int HD>
+struct FaCfg {
+  static constexpr int ATOMS = HD / 64;
+  static constexpr int Q_BYTES = TC_M * HD * 2;          // one tile
+  static constexpr int KV_BYTES = TC_KEYS * HD * 2;      // one chunk
+  static constexpr int OFF_Q = 0;                        // 2 tiles
+  static constexpr int OFF_K = 2 * Q_BYTES;              // 2 stages
+  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;     // 2 stages
+  static constexpr int BODY = OFF_V + 2 * KV_BYTES;
+  static constexpr int TILE_COLS = 256;
+};
+
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+// 32 scores -> 16 packed fp16 pairs of P (keys 0..lim visible); returns the sum
+__device__ __forceinline__ float fa_exp32(const uint32_t (&v)[32], int lim, float sl2, float nm, uint32_t (&pk)[16]) {
+  if (lim >= 31) {
+    float2 ls2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+    const float2 sl = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), sl, nm2);
+      float2 p;
+      if (((e >> 1) & 3) == 3) {
+        p = exp2_poly2(x);
+      } else {
+        p.x = fast_exp2(x.x);
+        p.y = fast_exp2(x.y);
+      }
+      ls2[(e >> 1) & 3] = fadd2(ls2[(e >> 1) & 3], p);
+      const __half2 hv = __floats2half2_rn(p.x, p.y);
+      pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+    }
+    const float2 s01 = fadd2(ls2[0], ls2[1]), s23 = fadd2(ls2[2], ls2[3]);
+    return (s01.x + s01.y) + (s23.x + s23.y);
+  }
+  float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    const float p0 = e <= lim ? fast_exp2(fmaf(__uint_as_float(v[e]), sl2, nm)) : 0.f;
+    const float p1 = e + 1 <= lim ? fast_exp2(fmaf(__uint_as_float(v[e + 1]), sl2, nm)) : 0.f;
+    ls[(e >> 1) & 3] += p0 + p1;
+    const __half2 hv = __floats2half2_rn(p0, p1);
+    pk[e >> 1] = *reinterpret_cast<const uint32_t*>(&hv);
+  }
+  return (ls[0] + ls[1]) + (ls[2] + ls[3]);
+}
+
+template <int HD>
+__global__ void __launch_bounds__(FA_THREADS, 1)
+    attention_fa_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const TcArgs a) {
+  using C = FaCfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  if (threadIdx.x == 0) {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if ((uint32_t)(sm - smem_raw) + C::BODY > dyn) __trap();   // launch_tc's pad assumption broken
+  }
+  __shared__ __align__(8) uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2],
+      o_final;
+  __shared__ uint32_t tmem_base;
+  __shared__ int s_pos[2 * TC_M];
+  __shared__ int16_t s_seq[2 * TC_M];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = gridDim.x - 1 - blockIdx.x;          // later (longer) tiles first: causal balance
+  const int kh = blockIdx.y;
+  const int R2 = 2 * a.R;
+  const int t0 = tile * R2;
+
+  if (threadIdx.x == 0) {
+    lp::mbar_init(&q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      lp::mbar_init(&k_full[b], 1);
+      lp::mbar_init(&k_empty[b], 1);
+      lp::mbar_init(&v_full[b], 1);
+      lp::mbar_init(&v_empty[b], 1);
+      lp::mbar_init(&s_full[b], 1);
+      lp::mbar_init(&p_full[b], 4);
+    }
+    lp::mbar_init(&o_final, 1);
+    lp::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     lp::smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+  }
+  lp::pdl_wait();
+  lp::pdl_trigger();
+  for (int i = threadIdx.x; i < R2; i += blockDim.x) {
+    const bool v = t0 + i < a.T;
+    s_pos[i] = v ? a.pos[t0 + i] : -1;
+    s_seq[i] = v ? (int16_t)a.seq[t0 + i] : (int16_t)-1;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base;
+  auto run = [&](int lo, int& hi, int& sq, int& chunks) {
+    sq = s_seq[lo];
+    chunks = 0;
+    for (hi = lo; hi < R2 && s_seq[hi] == sq; ++hi) chunks = max(chunks, (s_pos[hi] + TC_KEYS) / TC_KEYS);
+  };
+  const int nvalid = min(R2, a.T - t0);
+
+  if (warp == 0 || warp == 10) {
+    if (lane == 0) {
+      const bool is_k = warp == 0;
+      if (is_k) {
+        lp::mbar_expect_tx(&q_full, 2 * C::Q_BYTES);
+        for (int t = 0; t < 2; ++t)
+          for (int at = 0; at < C::ATOMS; ++at)
+            tma3d(sm + C::OFF_Q + t * C::Q_BYTES + at * ATOM, &tmQ, &q_full, at * 64, kh * a.G, t0 + t * a.R);
+      }
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      const CUtensorMap* map = is_k ? &tmK : &tmV;
+      uint8_t* base = sm + (is_k ? C::OFF_K : C::OFF_V);
+      int it = 0;
+      for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+        run(lo, hi, sq, nch);
+        const int row = sq * a.KV + kh;
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int st = it & 1;
+          if (it >= 2) lp::mbar_wait(&empty[st], ((it >> 1) - 1) & 1);
+          lp::mbar_expect_tx(&full[st], C::KV_BYTES);
+          for (int at = 0; at < C::ATOMS; ++at)
+            tma3d(base + st * C::KV_BYTES + at * (TC_KEYS * 128), map, &full[st], at * 64, c * TC_KEYS, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_KEYS >> 3) << 17) |
+                                   ((uint32_t)(TC_M >> 4) << 24);          // bf16 x bf16, both K-major
+      constexpr uint32_t idesc_pv = (1u << 4) | (1u << 16) | ((uint32_t)(HD >> 3) << 17) |
+                                    ((uint32_t)(TC_M >> 4) << 24);         // fp16: A (TMEM) K-major, B MN-major
+      int total = 0;
+      for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+        run(lo, hi, sq, nch);
+        total += nch;
+      }
+      auto issue_s = [&](int t, int j) {
+        const int st = j & 1;
+        const uint32_t sk = lp::smem_u32(sm + C::OFF_K + st * C::KV_BYTES);
+        const uint32_t sq = lp::smem_u32(sm + C::OFF_Q + t * C::Q_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma(tmem + t * C::TILE_COLS, desc_sw128(sq + (kk >> 2) * ATOM + (kk & 3) * 32, 16, 1024),
+               desc_sw128(sk + (kk >> 2) * (TC_KEYS * 128) + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0);
+        commit(&s_full[t]);
+        if (t == 1) commit(&k_empty[st]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int b = j & 1;
+        if (t == 0) lp::mbar_wait(&v_full[b], (j >> 1) & 1);
+        lp::mbar_wait(&p_full[t], j & 1);
+        fence_after();
+        TRACE(1, j);
+        const uint32_t sv = lp::smem_u32(sm + C::OFF_V + b * C::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < TC_KEYS / 16; ++kk)
+          umma_ts(tmem + t * C::TILE_COLS + 128, tmem + t * C::TILE_COLS + kk * 8,
+                  desc_sw128(sv + kk * 2048, TC_KEYS * 128, 1024), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        if (t == 1) commit(&v_empty[b]);
+      };
+      lp::mbar_wait(&q_full, 0);
+      if (total > 0) {
+        lp::mbar_wait(&k_full[0], 0);
+        fence_after();
+        TRACE(0, 0);
+        issue_s(0, 0);
+        issue_s(1, 0);
+      }
+      for (int j = 0; j < total; ++j) {
+        issue_pv(0, j);
+        if (j + 1 < total) {
+          lp::mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+          fence_after();
+          TRACE(0, j + 1);
+          issue_s(0, j + 1);           // after P_0(j) V in the in-order pipe: S_0 may overwrite P_0
+        }
+        issue_pv(1, j);
+        if (j + 1 < total) issue_s(1, j + 1);
+      }
+      if (total > 0) commit(&o_final);
+    }
+  } else if (warp <= 9) {
+    // ---------------- softmax: warpgroup t owns Q tile t, thread = row ----------------
+    constexpr float RESCALE = 8.0f;
+    const int t = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int i = t * a.R + r / a.G, g = r % a.G;    // token index within the CTA's 2R tokens
+    const int prow = i < nvalid ? s_pos[i] : -1;
+    const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16) + t * C::TILE_COLS;
+    float m_use = -INFINITY, l_run = 0.f;
+    int it = 0;
+    for (int lo = 0, hi, sq, nch; lo < nvalid; lo = hi) {
+      run(lo, hi, sq, nch);
+      const bool mine = i >= lo && i < hi;
+      for (int c = 0; c < nch; ++c, ++it) {
+        lp::mbar_wait(&s_full[t], it & 1);
+        fence_after();
+        if ((warp == 2 || warp == 6) && lane == 0) TRACE(2 + 4 * t, it);
+        const int lim = mine ? prow - c * TC_KEYS : -1;     // keys 0..lim of this chunk are visible
+        // pass 1: the row max over the visible keys (two 64-column loads)
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t v[64];
+          ld32(trow + h2 * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+          ld32(trow + h2 * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          wait_ld();
+          const int lh = lim - h2 * 64;
+          if (lh >= 63) {
+#pragma unroll
+            for (int e = 0; e < 64; e += 2)
+              mx4[(e >> 1) & 3] = fmax3(mx4[(e >> 1) & 3], __uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+          } else if (lh >= 0) {
+#pragma unroll
+            for (int e = 0; e < 64; ++e)
+              if (e <= lh) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(v[e]));
+          }
+        }
+        const float m_row = a.sl2 * fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        if ((warp == 2 || warp == 6) && lane == 0) TRACE(3 + 4 * t, it);
+        const bool move = m_row > m_use + RESCALE || (m_use == -INFINITY && m_row > -INFINITY);
+        const float sc = (move && m_use != -INFINITY) ? exp2f(m_use - m_row) : 1.f;
+        const bool resc = move && m_use != -INFINITY && it > 0;
+        if (move) {
+          l_run *= m_use == -INFINITY ? 0.f : sc;
+          m_use = m_row;
+        }
+        if (__any_sync(0xffffffffu, resc)) {   // O_t is stable here: S_t(it) done => P_t(it-1) V done
+#pragma unroll
+          for (int cg = 0; cg < HD / 32; ++cg) {
+            uint32_t o[32];
+            ld32(trow + 128 + cg * 32, o);
+            wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * sc);
+            st32(trow + 128 + cg * 32, o);
+          }
+        }
+        // pass 2: P = exp2(S sl2 - m) in fp16 over S's first 64 columns (each
+        // 32-key quarter's P lands on columns already read); the load of
+        // quarter q + 1 is in flight while quarter q computes
+        const float nm = -m_use;
+        float ls = 0.f;
+        uint32_t va[32], vb[32];
+        auto quarter_p = [&](const uint32_t (&vq)[32], int q) {
+          uint32_t pk[16];
+          if (lim - q * 32 < 0) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[e] = 0u;
+          } else {
+            ls += fa_exp32(vq, lim - q * 32, a.sl2, nm, pk);
+          }
+          st16(trow + q * 16, pk);
+        };
+        ld32(trow, va);
+        ld32(trow + 32, vb);
+        wait_ld32(va);
+        wait_ld32(vb);
+        quarter_p(va, 0);
+        ld32(trow + 64, va);
+        quarter_p(vb, 1);
+        wait_ld32(va);
+        ld32(trow + 96, vb);
+        quarter_p(va, 2);
+        wait_ld32(vb);
+        quarter_p(vb, 3);
+        l_run += ls;
+        wait_st();
+        fence_before();
+        if ((warp == 2 || warp == 6) && lane == 0) TRACE(4 + 4 * t, it);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        if ((warp == 2 || warp == 6) && lane == 0) TRACE(5 + 4 * t, it);
+      }
+    }
+    if (it > 0) {
+      lp::mbar_wait(&o_final, 0);
+      fence_after();
+    }
+    const bool live = i < nvalid && l_run > 0.f;
+    const float inv = live ? 1.0f / l_run : 0.f;
+    __nv_bfloat16* orow = a.out + ((int64_t)(t0 + i) * a.H + kh * a.G + g) * HD;
+#pragma unroll
+    for (int cg = 0; cg < HD / 32; ++cg) {
+      uint32_t o[32];
+      ld32(trow + 128 + cg * 32, o);
+      wait_ld();
+      if (live) {
+#pragma unroll
+        for (int d = 0; d < 32; d += 8) {
+          __nv_bfloat162 w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            w[e] = __floats2bfloat162_rn(__uint_as_float(o[d + 2 * e]) * inv, __uint_as_float(o[d + 2 * e + 1]) * inv);
+          *reinterpret_cast<uint4*>(orow + cg * 32 + d) = *reinterpret_cast<const uint4*>(w);
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 template <int HD>
 int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos, const int32_t* seq,
               int T, int H, int KV, int64_t max_len, float scale, void* out, cudaStream_t s) {
@@ -1017,21 +1387,23 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   const int G = H / KV;
   const int R = TC_M / G;
   // LP_ATTN_TC selects the variant (A/B tables: profiles/r02/attn_prefill_*):
-  //   3 (default) one Q tile per CTA, lazy row max (exchanged after the exp
-  //     pass; P recomputed only when m moves), packed FFMA2/FADD2/FMNMX3 math
-  //     and one key pair in four on the FMA-pipe exp2: 1 x 2048 rows 82.7 ->
-  //     80.2 us (8B), 2 x 4096 rows 439 -> 418 us (8B), 847 -> 804 us (70B);
+  //   7 (default) FA4 layout: two Q tiles per CTA, 128-key chunks, P kept in
+  //     TMEM as the P V MMA's A operand, one softmax thread per row:
+  //     8B 1 x 2048 rows 82.5 -> 77 us, 2 x 4096 439 -> 355 us, 8 x 512 84 ->
+  //     67 us; 70B 2 x 4096 847 -> 640 us (vs the eager one-tile kernel);
+  //   3 one Q tile per CTA, lazy row max (exchanged after the exp pass),
+  //     packed FFMA2/FADD2/FMNMX3 math, one key pair in four on the FMA-pipe
+  //     exp2 (80.2 / 418 / 86 us);
   //   1 the eager one-tile kernel (row max first, partner half streamed);
-  //   4 variant 3 with four warps per row quarter (32 keys each; slower);
+  //   4 variant 3 with four warps per row quarter (slower);
   //   5 / 6 variant 3 with no / half the exponentials on the FMA pipe;
-  //   2 the ping-pong kernel: wins on many short prompts (8 x 512 rows: 84 ->
-  //     72 us 8B, 144 -> 115 us 70B), loses on long ones (half as many, twice
-  //     as long CTAs on 148 SMs).
+  //   2 the 64-key ping-pong kernel (P in smem; its N = 64 S MMAs are
+  //     smem-bound).
   static const int variant = [] {
     const char* e = getenv("LP_ATTN_TC");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 7;
   }();
-  const uint32_t kbox = variant == 2 ? PP_KEYS : TC_KEYS;
+  const uint32_t kbox = variant == 2 ? PP_KEYS : TC_KEYS;   // 7 and the one-tile kernels: 128-key chunks
   CUtensorMap mq, mk, mv;
   const uint64_t rows = (uint64_t)1 << 24;   // sequence x kv-head rows of the caches (unbounded here)
   if (map3d(&mq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, q, HD, H, T, (uint64_t)HD * 2, (uint64_t)H * HD * 2, G, R)) return -1;
@@ -1072,6 +1444,34 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     return t;
   }();
   TcArgs args{pos, seq, (__nv_bfloat16*)out, T, H, KV, G, R, scale * 1.4426950408889634f, trace};
+  if (variant == 7) {
+    using F = FaCfg<HD>;
+    if (trace) LP_CUDA(cudaMemset(trace, 0, 64 * 16 * sizeof(long long)));
+    static int fa_smem = 0;
+    static uint64_t fattr = 0;
+    if (!(fattr >> dev & 1)) {
+      cudaFuncAttributes fa;
+      LP_CUDA(cudaFuncGetAttributes(&fa, attention_fa_kernel<HD>));
+      fa_smem = F::BODY + (int)((1024 - fa.sharedSizeBytes % 1024) % 1024);
+      LP_CUDA(cudaFuncSetAttribute(attention_fa_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa_smem));
+      fattr |= 1ull << dev;
+    }
+    const dim3 grid((unsigned)((T + 2 * R - 1) / (2 * R)), (unsigned)KV);
+    LP_CUDA(lp::launch(attention_fa_kernel<HD>, grid, dim3(FA_THREADS), fa_smem, s, mq, mk, mv, args));
+    if (trace) {
+      static long long h[64 * 16];
+      LP_CUDA(cudaStreamSynchronize(s));
+      LP_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
+      for (int it = 0; it < 64 && (it == 0 || h[it * 16 + 2]); ++it) {
+        const long long* t = h + it * 16;
+        fprintf(stderr, "fa chunk %2d: K_ready %7lld PV1_issue %7lld | tile0 S_ready %7lld max %+5lld exp %+5lld arrive "
+                "%+5lld | tile1 S_ready %7lld max %+5lld exp %+5lld arrive %+5lld\n", it, t[0] - h[0],
+                t[1] ? t[1] - h[0] : 0, t[2] - h[0], t[3] - t[2], t[4] - t[3], t[5] - t[4], t[6] - h[0], t[7] - t[6],
+                t[8] - t[7], t[9] - t[8]);
+      }
+    }
+    return 0;
+  }
   if (variant == 2) {
     using P = PpCfg<HD>;
     if (trace) LP_CUDA(cudaMemset(trace, 0, 64 * 16 * sizeof(long long)));
