@@ -1073,6 +1073,7 @@ __device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
       : "memory");
 }
 // 32 scores -> 16 packed fp16 pairs of P (keys 0..lim visible); returns the sum
+template <int POLY>
 __device__ __forceinline__ float fa_exp32(const uint32_t (&v)[32], int lim, float sl2, float nm, uint32_t (&pk)[16]) {
   if (lim >= 31) {
     float2 ls2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
@@ -1081,7 +1082,7 @@ __device__ __forceinline__ float fa_exp32(const uint32_t (&v)[32], int lim, floa
     for (int e = 0; e < 32; e += 2) {
       const float2 x = ffma2(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), sl, nm2);
       float2 p;
-      if (((e >> 1) & 3) == 3) {
+      if (((e >> 1) & 3) >= 4 - POLY) {      // POLY of every 4 key pairs on the FMA pipe
         p = exp2_poly2(x);
       } else {
         p.x = fast_exp2(x.x);
@@ -1106,7 +1107,7 @@ __device__ __forceinline__ float fa_exp32(const uint32_t (&v)[32], int lim, floa
   return (ls[0] + ls[1]) + (ls[2] + ls[3]);
 }
 
-template <int HD>
+template <int HD, int POLY = 1>
 __global__ void __launch_bounds__(FA_THREADS, 1)
     attention_fa_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const TcArgs a) {
@@ -1272,23 +1273,21 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         fence_after();
         if ((warp == 2 || warp == 6) && lane == 0) TRACE(2 + 4 * t, it);
         const int lim = mine ? prow - c * TC_KEYS : -1;     // keys 0..lim of this chunk are visible
-        // pass 1: the row max over the visible keys (two 64-column loads)
+        // pass 1: the row max over the visible keys (one TMEM round trip)
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        {
+          uint32_t v[128];
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          uint32_t v[64];
-          ld32(trow + h2 * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
-          ld32(trow + h2 * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          for (int q = 0; q < 4; ++q) ld32(trow + q * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * q));
           wait_ld();
-          const int lh = lim - h2 * 64;
-          if (lh >= 63) {
+          if (lim >= 127) {
 #pragma unroll
-            for (int e = 0; e < 64; e += 2)
+            for (int e = 0; e < 128; e += 2)
               mx4[(e >> 1) & 3] = fmax3(mx4[(e >> 1) & 3], __uint_as_float(v[e]), __uint_as_float(v[e + 1]));
-          } else if (lh >= 0) {
+          } else if (lim >= 0) {
 #pragma unroll
-            for (int e = 0; e < 64; ++e)
-              if (e <= lh) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(v[e]));
+            for (int e = 0; e < 128; ++e)
+              if (e <= lim) mx4[e & 3] = fmaxf(mx4[e & 3], __uint_as_float(v[e]));
           }
         }
         const float m_row = a.sl2 * fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
@@ -1316,29 +1315,31 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         // quarter q + 1 is in flight while quarter q computes
         const float nm = -m_use;
         float ls = 0.f;
-        uint32_t va[32], vb[32];
-        auto quarter_p = [&](const uint32_t (&vq)[32], int q) {
-          uint32_t pk[16];
+        uint32_t va[32], vb[32], pk[32];
+        // P of quarter q into pk[16 h .. 16 h + 15]
+        auto quarter_p = [&](const uint32_t (&vq)[32], int q, int h) {
+          uint32_t (&ph)[16] = *reinterpret_cast<uint32_t(*)[16]>(pk + 16 * h);
           if (lim - q * 32 < 0) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) pk[e] = 0u;
+            for (int e = 0; e < 16; ++e) ph[e] = 0u;
           } else {
-            ls += fa_exp32(vq, lim - q * 32, a.sl2, nm, pk);
+            ls += fa_exp32<POLY>(vq, lim - q * 32, a.sl2, nm, ph);
           }
-          st16(trow + q * 16, pk);
         };
         ld32(trow, va);
         ld32(trow + 32, vb);
         wait_ld32(va);
         wait_ld32(vb);
-        quarter_p(va, 0);
+        quarter_p(va, 0, 0);
         ld32(trow + 64, va);
-        quarter_p(vb, 1);
+        quarter_p(vb, 1, 1);
+        st32(trow, pk);                  // P keys 0..63 -> columns 0..31 (S keys 0..31, read)
         wait_ld32(va);
         ld32(trow + 96, vb);
-        quarter_p(va, 2);
+        quarter_p(va, 2, 0);
         wait_ld32(vb);
-        quarter_p(vb, 3);
+        quarter_p(vb, 3, 1);
+        st32(trow + 32, pk);             // P keys 64..127 -> columns 32..63 (S keys 32..63, read)
         l_run += ls;
         wait_st();
         fence_before();
@@ -1447,17 +1448,35 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   if (variant == 7) {
     using F = FaCfg<HD>;
     if (trace) LP_CUDA(cudaMemset(trace, 0, 64 * 16 * sizeof(long long)));
-    static int fa_smem = 0;
+    static int fa_smem[3] = {0, 0, 0};
     static uint64_t fattr = 0;
-    if (!(fattr >> dev & 1)) {
+    auto fa_attr = [](auto kern) -> int {
       cudaFuncAttributes fa;
-      LP_CUDA(cudaFuncGetAttributes(&fa, attention_fa_kernel<HD>));
-      fa_smem = F::BODY + (int)((1024 - fa.sharedSizeBytes % 1024) % 1024);
-      LP_CUDA(cudaFuncSetAttribute(attention_fa_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa_smem));
+      if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return -1;
+      const int bytes = F::BODY + (int)((1024 - fa.sharedSizeBytes % 1024) % 1024);
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return -1;
+      return bytes;
+    };
+    if (!(fattr >> dev & 1)) {
+      fa_smem[0] = fa_attr(attention_fa_kernel<HD, 1>);
+      fa_smem[1] = fa_attr(attention_fa_kernel<HD, 0>);
+      fa_smem[2] = fa_attr(attention_fa_kernel<HD, 2>);
+      LP_CHECK(fa_smem[0] > 0 && fa_smem[1] > 0 && fa_smem[2] > 0, "attention_fa: smem attributes: %s",
+               cudaGetErrorString(cudaGetLastError()));
       fattr |= 1ull << dev;
     }
+    // LP_ATTN_FA_POLY: key pairs in four on the FMA-pipe exp2 (1 default; 0, 2 for A/B)
+    static const int poly = [] {
+      const char* e = getenv("LP_ATTN_FA_POLY");
+      return e ? atoi(e) : 1;
+    }();
     const dim3 grid((unsigned)((T + 2 * R - 1) / (2 * R)), (unsigned)KV);
-    LP_CUDA(lp::launch(attention_fa_kernel<HD>, grid, dim3(FA_THREADS), fa_smem, s, mq, mk, mv, args));
+    if (poly == 0)
+      LP_CUDA(lp::launch(attention_fa_kernel<HD, 0>, grid, dim3(FA_THREADS), fa_smem[1], s, mq, mk, mv, args));
+    else if (poly == 2)
+      LP_CUDA(lp::launch(attention_fa_kernel<HD, 2>, grid, dim3(FA_THREADS), fa_smem[2], s, mq, mk, mv, args));
+    else
+      LP_CUDA(lp::launch(attention_fa_kernel<HD, 1>, grid, dim3(FA_THREADS), fa_smem[0], s, mq, mk, mv, args));
     if (trace) {
       static long long h[64 * 16];
       LP_CUDA(cudaStreamSynchronize(s));
