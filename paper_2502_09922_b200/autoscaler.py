@@ -82,6 +82,8 @@ class AutoscaleServer(Server):
         self.cfg = CONFIGS[model] if isinstance(model, str) else model
         self.lay = build_layout(self.cfg, block_count)
         self.local_slots, self.max_len, self.use_graphs = local_slots, max_len, use_graphs
+        self.pipeline_batch = 1                                    # the reference's pipeline capacity
+        self.pipeline_prefill_tokens = self.prefill_budget(self.lay)
         self.prefill_ms_per_token = model_spec(self.cfg).prefill_ms_per_token
         self.policy = policy or AutoscalePolicy()
         self.k = k

@@ -107,6 +107,14 @@ class Server:
 
     PREFILL_PASS_FLOP = 8.2e12     # pipeline prefill budget per pass (see __init__)
 
+    @classmethod
+    def prefill_budget(cls, layout, tokens=None) -> int:
+        """Prompt tokens one pipeline pass prefills: ``tokens``, else
+        PREFILL_PASS_FLOP of prompt (2 FLOP per parameter per token)."""
+        if tokens is None:
+            tokens = cls.PREFILL_PASS_FLOP / (2.0 * layout.weights_bytes / 2)
+        return max(1, int(tokens))
+
     def __init__(self, plan, cluster, local_slots: int = 8, max_len: int = 512, switch_hold_tokens: int = 0,
                  prefill_ms_per_token: float = 0.5, use_graphs: bool = True, pipeline_batch: int = 1,
                  pipeline_prefill_tokens: int | None = None):
@@ -135,9 +143,7 @@ class Server:
         self.use_graphs = use_graphs
         self.prefill_ms_per_token = prefill_ms_per_token
         self.pipeline_batch = max(1, int(pipeline_batch))
-        if pipeline_prefill_tokens is None:
-            pipeline_prefill_tokens = self.PREFILL_PASS_FLOP / (2.0 * plan.layout.weights_bytes / 2)
-        self.pipeline_prefill_tokens = max(1, int(pipeline_prefill_tokens))
+        self.pipeline_prefill_tokens = self.prefill_budget(plan.layout, pipeline_prefill_tokens)
         self.events = []
         self.profile = []          # per iteration: (start, enqueue s, device s, tokens, unit batches)
         self.profile_detail = [] if os.environ.get("LP_SERVE_PROFILE") else None

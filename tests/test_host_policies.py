@@ -96,3 +96,19 @@ def test_fit_ctas_shares_one_device(monkeypatch):
     assert E._fit_ctas(0, 74, 1, 1) == (1, 1)
     with pytest.raises(ValueError):
         E._fit_ctas(0, 200, 0, 1)
+
+
+def test_pipeline_prefill_budget():
+    """Pipeline passes prefill ~8.2 TFLOP of prompt: 510 tokens for
+    Llama-3-8B, fewer than one 128-token prompt for 70B (so one request per
+    pass); an explicit budget wins.  AutoscaleServer sets the same budget
+    (it does not run Server.__init__)."""
+    import inspect
+    from paper_2502_09922_b200 import autoscaler as A
+    from paper_2502_09922_b200 import image as I
+    from paper_2502_09922_b200.serving import Server
+    assert Server.prefill_budget(I.build_layout(I.CONFIGS["llama3-8b"], 16)) == 510
+    assert Server.prefill_budget(I.build_layout(I.CONFIGS["llama3-70b"], 16)) < 128
+    assert Server.prefill_budget(I.build_layout(I.CONFIGS["llama3-8b"], 16), 64) == 64
+    src = inspect.getsource(A.AutoscaleServer.__init__)
+    assert "pipeline_prefill_tokens" in src and "pipeline_batch" in src
