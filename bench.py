@@ -19,7 +19,7 @@ reference's λPipe binomial schedule at EVERY N.  Receivers are overwritten
 with a byte pattern before every step (untimed), so each step's checksums
 prove that step delivered the model.  At N >= 2 the line also carries
 "sharded_host" (our non-reference host-load plan, labelled as such) and the
-GPU-sourced multicast (Llama-3-8B, GPU0 -> N-1 peers, b = 32; BASELINE
+GPU-sourced multicast (Llama-3-8B, GPU0 -> N-1 peers, b = 16; BASELINE
 configs[1] at N = 8) as "gpu_source"; at N >= 3 "execute_while_load"
 (Llama-3-8B, 2 GPU sources, λPipe pipelines serving a burst while the rest
 receive; tokens/s + TTFT), at N >= 4 "execute_while_load_70b" (BASELINE
@@ -56,8 +56,10 @@ sys.path.insert(0, ROOT)
 METRIC = "scale-out time & aggregate GB/s (1→N GPUs); tokens/s + TTFT during load"
 C3_MODEL, C3_BLOCKS = "llama2-13b", 40
 C2_MODEL, C2_BLOCKS = "llama3-8b", 16     # serving (execute-while-load) plan
-C2_MC_BLOCKS = 32                          # GPU-sourced multicast: (b + log2 N - 1) / b pipeline fill
-                                           # 23.67 ms (b=32) vs 24.04 ms (b=16) at N=4 on the copy engines
+C2_MC_BLOCKS = 16                          # GPU-sourced multicast: measured best at N = 4 (0.675 vs 0.642 at
+                                           # b = 32, profiles/r02/mc_gpu_source_n4_blocks.txt); the reference
+                                           # planner's elbow is 10 (N = 4) / 14 (N = 8); round 1's copy
+                                           # engines preferred 32 on one box (23.67 vs 24.04 ms)
 SEED = 20250815
 NCU_TRAFFIC_RATIO = (3.153332e9 + 10.150656e6) / 3193006080   # profiles/mc_kernel_host_pull_full_r01.csv
 
