@@ -202,7 +202,9 @@ int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim,
  * (multiple of 32), H/KV <= 8.  T*KV >= 1024 (prefill), head_dim 64/128,
  * max_len > 256:
  * tcgen05/TMEM kernel (128-row tiles of R tokens x H/KV heads, TMA-fed,
- * fp32 S and O in TMEM; LP_ATTN_TC=0 selects the mma.sync kernel); decode:
+ * two tiles per CTA, fp32 S and O in TMEM, fp16 P kept in TMEM as the P.V
+ * MMA's A operand; LP_ATTN_TC selects the other variants, 0 = mma.sync);
+ * decode:
  * mma.sync kernels (few rows, K/V streaming bound; long caches split keys
  * over a thread-block cluster); other head sizes: CUDA-core online softmax. */
 int lp_attention(const void* q, const void* k_cache, const void* v_cache, const int32_t* pos,
