@@ -84,6 +84,11 @@ typedef struct lp_mc lp_mc;
 #define LP_NODE_HOST 1
 int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_off,
                  const int64_t* block_len, int64_t tile_bytes);
+/* lp_mc_create with a tile size per block (the split executor: copy-engine
+ * blocks in large tiles, in-kernel blocks in small ones); the smallest tile
+ * bounds lp_mc_configure's chunk */
+int lp_mc_create_tiled(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_off,
+                       const int64_t* block_len, const int64_t* block_tile);
 int lp_mc_destroy(lp_mc* mc);
 /* bytes of the per-node signal area (tile flags, block counters, arrivals) */
 int lp_mc_signal_bytes(const lp_mc* mc, int64_t* bytes);

@@ -49,6 +49,7 @@ SIGNATURES = {
     "lp_fill_tensors": [_vp, C.c_int, _P(_i64), _P(_i64), _P(_i32), _P(_i32), _u64, _vp],
     "lp_block_checksums": [_vp, C.c_int, _P(_i64), _P(_i64), _P(_u64), _vp],
     "lp_mc_create": [_P(_vp), C.c_int, C.c_int, _P(_i64), _P(_i64), _i64],
+    "lp_mc_create_tiled": [_P(_vp), C.c_int, C.c_int, _P(_i64), _P(_i64), _P(_i64)],
     "lp_mc_destroy": [_vp],
     "lp_mc_signal_bytes": [_vp, _P(_i64)],
     "lp_mc_set_node": [_vp, C.c_int, C.c_int, _vp, _vp, _vp],

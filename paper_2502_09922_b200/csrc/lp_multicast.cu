@@ -43,6 +43,7 @@ struct NodeDev {
 struct BlockDev {
   int64_t off;
   int64_t len;
+  int64_t tile;       // bytes per tile of this block (uniform unless lp_mc_create_tiled)
   int32_t tile_base;
   int32_t ntiles;
 };
@@ -188,8 +189,8 @@ __device__ void ldg_role(const McParams& p, int ob, int oe, int lane, int lanes,
     const BlockDev bl = p.blocks[op.block];
     const NodeDev src = p.nodes[op.src];
     const NodeDev dst = p.nodes[op.dst];
-    const int64_t lo = (int64_t)t * p.tile_bytes;
-    const int64_t n = min(p.tile_bytes, bl.len - lo);
+    const int64_t lo = (int64_t)t * bl.tile;
+    const int64_t n = min(bl.tile, bl.len - lo);
     copy_tile(src.image + bl.off + lo, dst.image + bl.off + lo, n, p.wide_loads != 0);
     __syncthreads();  // every thread's stores of this tile precede the flag
     if (threadIdx.x == 0) {
@@ -307,8 +308,8 @@ __device__ void tma_role(const McParams& p, int ob, int oe, int lane, int lanes,
         }
         lp::fence_proxy_async_global();  // order the acquire before async-proxy reads
       }
-      const int64_t tlo = (int64_t)g.t * p.tile_bytes;
-      const int64_t tlen = min(p.tile_bytes, bl.len - tlo);
+      const int64_t tlo = (int64_t)g.t * bl.tile;
+      const int64_t tlen = min(bl.tile, bl.len - tlo);
       const uint32_t nb = (uint32_t)min((int64_t)chunk, tlen - g.c);
       const int slot = (int)(q_load % kStages);
       if (q_load >= kStages) lp::bulk_wait_read_n((int)(q_store - 1 - (q_load - kStages)));
@@ -595,14 +596,19 @@ static int compile(lp_mc* mc) {
 
 extern "C" {
 
-int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_off,
-                 const int64_t* block_len, int64_t tile_bytes) {
-  LP_CHECK(out && n_nodes >= 1 && n_nodes <= 4096 && n_blocks >= 1, "lp_mc_create: bad arguments");
-  LP_CHECK(tile_bytes >= 4096 && tile_bytes % 16 == 0, "lp_mc_create: tile_bytes must be >=4096 and a multiple of 16");
+int lp_mc_create_tiled(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_off,
+                       const int64_t* block_len, const int64_t* block_tile) {
+  LP_CHECK(out && n_nodes >= 1 && n_nodes <= 4096 && n_blocks >= 1 && block_tile, "lp_mc_create: bad arguments");
+  int64_t min_tile = INT64_MAX;
+  for (int i = 0; i < n_blocks; ++i) {
+    LP_CHECK(block_tile[i] >= 4096 && block_tile[i] % 16 == 0,
+             "lp_mc_create: tile bytes must be >= 4096 and a multiple of 16 (block %d)", i);
+    min_tile = std::min(min_tile, block_tile[i]);
+  }
   lp_mc* mc = new lp_mc();
   mc->n_nodes = n_nodes;
   mc->n_blocks = n_blocks;
-  mc->tile_bytes = tile_bytes;
+  mc->tile_bytes = min_tile;         // the smallest tile bounds the kernel's chunk size
   int64_t tiles = 0;
   for (int i = 0; i < n_blocks; ++i) {
     if (block_off[i] % 16 || block_len[i] % 16 || block_len[i] <= 0) {
@@ -610,8 +616,8 @@ int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_of
       lp::set_error("lp_mc_create: block %d offset/length must be positive multiples of 16", i);
       return -2;
     }
-    int64_t nt = (block_len[i] + tile_bytes - 1) / tile_bytes;
-    mc->blocks.push_back(BlockDev{block_off[i], block_len[i], (int32_t)tiles, (int32_t)nt});
+    int64_t nt = (block_len[i] + block_tile[i] - 1) / block_tile[i];
+    mc->blocks.push_back(BlockDev{block_off[i], block_len[i], block_tile[i], (int32_t)tiles, (int32_t)nt});
     tiles += nt;
   }
   mc->total_tiles = tiles;
@@ -638,6 +644,13 @@ int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_of
   cudaFuncGetAttributes(&fa, count_reset_kernel);
   *out = mc;
   return 0;
+}
+
+int lp_mc_create(lp_mc** out, int n_nodes, int n_blocks, const int64_t* block_off,
+                 const int64_t* block_len, int64_t tile_bytes) {
+  LP_CHECK(n_blocks >= 1, "lp_mc_create: bad arguments");
+  std::vector<int64_t> tiles((size_t)n_blocks, tile_bytes);
+  return lp_mc_create_tiled(out, n_nodes, n_blocks, block_off, block_len, tiles.data());
 }
 
 int lp_mc_destroy(lp_mc* mc) {
@@ -847,8 +860,8 @@ static int enqueue_ce(lp_mc* mc, int node, uint32_t epoch, const std::vector<int
     const NodeDev dst = mc->nodes[op.dst];
     CUstream s = (CUstream)streams[k % n_streams];
     for (int t = 0; t < bl.ntiles; ++t) {
-      const int64_t lo = (int64_t)t * mc->tile_bytes;
-      const int64_t n = std::min<int64_t>(mc->tile_bytes, bl.len - lo);
+      const int64_t lo = (int64_t)t * bl.tile;
+      const int64_t n = std::min<int64_t>(bl.tile, bl.len - lo);
       if (op.wait) {
         CUresult r = cuStreamWaitValue32(s, (CUdeviceptr)(src.flags + bl.tile_base + t), epoch,
                                          CU_STREAM_WAIT_VALUE_GEQ);

@@ -60,7 +60,8 @@ def device_view(ptr: int, nbytes: int, device: int, dtype=None, shape=None):
 class MulticastEngine:
     """One compiled λPipe multicast over a fixed block table."""
 
-    def __init__(self, n_nodes: int, block_offsets, block_lengths, tile_bytes: int = DEFAULT_TILE):
+    def __init__(self, n_nodes: int, block_offsets, block_lengths, tile_bytes=DEFAULT_TILE):
+        """``tile_bytes``: one size, or one per block (lp_mc_create_tiled)."""
         lib = N.lib()
         self.n_nodes = n_nodes
         self.n_blocks = len(block_offsets)
@@ -68,8 +69,15 @@ class MulticastEngine:
         self.block_lengths = list(block_lengths)
         self.tile_bytes = tile_bytes
         h = C.c_void_p()
-        N.check(lib.lp_mc_create(C.byref(h), n_nodes, self.n_blocks, N.i64_array(block_offsets),
-                                 N.i64_array(block_lengths), tile_bytes), "lp_mc_create")
+        if isinstance(tile_bytes, (list, tuple)):
+            if len(tile_bytes) != self.n_blocks:
+                raise ValueError("one tile size per block")
+            N.check(lib.lp_mc_create_tiled(C.byref(h), n_nodes, self.n_blocks, N.i64_array(block_offsets),
+                                           N.i64_array(block_lengths), N.i64_array(tile_bytes)),
+                    "lp_mc_create_tiled")
+        else:
+            N.check(lib.lp_mc_create(C.byref(h), n_nodes, self.n_blocks, N.i64_array(block_offsets),
+                                     N.i64_array(block_lengths), tile_bytes), "lp_mc_create")
         self._h = h
         sb = C.c_int64()
         N.check(lib.lp_mc_signal_bytes(h, C.byref(sb)), "lp_mc_signal_bytes")
@@ -306,7 +314,7 @@ class Cluster:
 
     @classmethod
     def local(cls, n_gpu_nodes: int, block_offsets, block_lengths, image_bytes: int, device: int = 0,
-              host_node: bool = False, tile_bytes: int = DEFAULT_TILE):
+              host_node: bool = False, tile_bytes=DEFAULT_TILE):
         """All GPU nodes on one device (node ids 1.. if a host node 0 exists)."""
         n_nodes = n_gpu_nodes + (1 if host_node else 0)
         with on_device(device):
@@ -332,7 +340,7 @@ class Cluster:
 
     @classmethod
     def distributed(cls, block_offsets, block_lengths, image_bytes: int, host_node: bool = False,
-                    tile_bytes: int = DEFAULT_TILE, shm_name: str = "lambdapipe_host_image"):
+                    tile_bytes=DEFAULT_TILE, shm_name: str = "lambdapipe_host_image"):
         """One GPU node per torchrun rank (node id = rank, +1 with a host node 0)."""
         import torch
         import torch.distributed as dist
@@ -373,7 +381,7 @@ class Cluster:
 
     @classmethod
     def devices(cls, node_devices: list, block_offsets, block_lengths, image_bytes: int, host_node: bool = False,
-                tile_bytes: int = DEFAULT_TILE):
+                tile_bytes=DEFAULT_TILE):
         """One process driving several GPUs: GPU node i lives on device
         ``node_devices[i]`` (node ids shift by one if a host node 0 exists).
         An entry of -1 makes that node a HOST node instead (the box's
@@ -415,7 +423,7 @@ class Cluster:
         return cl
 
     @classmethod
-    def over_buffers(cls, buffers: list, block_offsets, block_lengths, tile_bytes: int = DEFAULT_TILE):
+    def over_buffers(cls, buffers: list, block_offsets, block_lengths, tile_bytes=DEFAULT_TILE):
         """An engine over EXISTING node buffers (no allocation, nothing freed
         on close): ``buffers[i]`` is the NodeBuffer of op-local node i.  Used
         by the autoscaling server, which keeps one image + signal area per GPU

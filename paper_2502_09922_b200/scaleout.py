@@ -328,6 +328,7 @@ def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
 
 CE_TILE = 256 << 20
 HYBRID_TILE = 64 << 20   # DMA tile of the PCIe hop = relay granule of the kernel
+SPLIT_CE_TILE = 64 << 20  # copy-engine blocks of the split executor
 
 
 def choose_strategy(host_source: bool, n_gpus: int) -> str:
@@ -380,6 +381,11 @@ class ScaleOut:
         if executor == "auto":
             executor, tile_bytes = choose_executor(plan, tile_bytes)
         lay = plan.layout
+        if executor == "split" and not isinstance(tile_bytes, (list, tuple)):
+            # per-executor tiling: the copy-engine blocks (b % 2 == 0) in
+            # SPLIT_CE_TILE tiles (few stream ops), the in-kernel ones in
+            # tile_bytes (a tile is one CTA's unit)
+            tile_bytes = [SPLIT_CE_TILE if b % 2 == 0 else tile_bytes for b in range(len(lay.block_offsets))]
         if distributed:
             self.cluster = E.Cluster.distributed(lay.block_offsets, lay.block_lengths, lay.weights_bytes,
                                                  host_node=plan.host_source, tile_bytes=tile_bytes)
