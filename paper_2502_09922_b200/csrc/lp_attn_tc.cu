@@ -1396,8 +1396,8 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   //     packed FFMA2/FADD2/FMNMX3 math, one key pair in four on the FMA-pipe
   //     exp2 (80.2 / 418 / 86 us);
   //   1 the eager one-tile kernel (row max first, partner half streamed);
-  //   4 variant 3 with four warps per row quarter (slower);
-  //   5 / 6 variant 3 with no / half the exponentials on the FMA pipe;
+  //   (measured and dropped: variant 3 with four warps per row quarter, or
+  //   with 0 / 2 of 4 key pairs on the FMA pipe: attn_prefill_lazy_ab.txt)
   //   2 the 64-key ping-pong kernel (P in smem; its N = 64 S MMAs are
   //     smem-bound).
   static const int variant = [] {
@@ -1425,14 +1425,11 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return -1;
     return bytes;
   };
-  static int tc_smem[5] = {0, 0, 0, 0, 0};
+  static int tc_smem[2] = {0, 0};
   if (!(attr >> dev & 1)) {
     tc_smem[0] = smem_for(attention_tc_kernel<HD, 2, false>);
     tc_smem[1] = smem_for(attention_tc_kernel<HD, 2, true>);
-    tc_smem[2] = HD == 128 ? smem_for(attention_tc_kernel<128, 4, true>) : 0;
-    tc_smem[3] = smem_for(attention_tc_kernel<HD, 2, true, 0>);
-    tc_smem[4] = smem_for(attention_tc_kernel<HD, 2, true, 2>);
-    LP_CHECK(tc_smem[0] > 0 && tc_smem[1] > 0 && tc_smem[2] >= 0, "attention_tc: smem attributes: %s",
+    LP_CHECK(tc_smem[0] > 0 && tc_smem[1] > 0, "attention_tc: smem attributes: %s",
              cudaGetErrorString(cudaGetLastError()));
     attr |= 1ull << dev;
   }
@@ -1515,13 +1512,7 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     return 0;
   }
   const dim3 grid((unsigned)((T + R - 1) / R), (unsigned)KV);
-  if (variant == 4 && HD == 128)
-    LP_CUDA(lp::launch(attention_tc_kernel<128, 4, true>, grid, dim3(19 * 32), tc_smem[2], s, mq, mk, mv, args));
-  else if (variant == 5)      // lazy, SFU only
-    LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, true, 0>, grid, dim3(11 * 32), tc_smem[3], s, mq, mk, mv, args));
-  else if (variant == 6)      // lazy, half the exponentials on the FMA pipe
-    LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, true, 2>, grid, dim3(11 * 32), tc_smem[4], s, mq, mk, mv, args));
-  else if (variant == 1)
+  if (variant == 1)
     LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, false>, grid, dim3(11 * 32), tc_smem[0], s, mq, mk, mv, args));
   else
     LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, true>, grid, dim3(11 * 32), tc_smem[1], s, mq, mk, mv, args));
