@@ -238,7 +238,10 @@ def test_generate_api_matches_oracle(tiny):
 
 @pytest.mark.parametrize("hd,H,KV,lens,cap", [(128, 32, 8, [1024], 0), (128, 64, 8, [700, 300], 0),
                                                (128, 8, 8, [517], 0), (64, 4, 2, [600, 1, 33], 0),
-                                               (128, 32, 8, [64] * 9 + [130], 400)])
+                                               (128, 32, 8, [64] * 9 + [130], 400),
+                                               # 70B groups (G = 8, 16-token tiles, 32 per CTA) with
+                                               # ragged lengths; MHA at head_dim 64
+                                               (128, 64, 8, [37, 250, 5, 301], 0), (64, 8, 8, [300, 77], 0)])
 def test_prefill_attention_tcgen05_causal(hd, H, KV, lens, cap):
     """Prompts laid out as consecutive rows (the serving layout: one or more
     sequences back to back, positions 0..len-1) through the tcgen05/TMEM
