@@ -318,8 +318,11 @@ __global__ void __launch_bounds__((3 + 4 * NS) * 32, 1)
   static_assert(NS == 2 || (LAZY && HD % (32 * NS) == 0), "4-way key split: lazy path, 32 O columns per warp");
   constexpr int VW = 2 + 4 * NS;               // the V producer warp (after the softmax warps)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = gridDim.x - 1 - blockIdx.x;          // later (longer) tiles first: causal balance
-  const int kh = blockIdx.y;
+  // 1-D grid over (tile, kv head), longest tiles of EVERY head first: the
+  // block scheduler then fills the SMs in LPT order (a [tiles, heads] grid
+  // launched head 0's short tiles before head 7's long ones)
+  const int tile = (int)(gridDim.x / a.KV) - 1 - (int)(blockIdx.x / a.KV);
+  const int kh = (int)(blockIdx.x % a.KV);
   const int t0 = tile * a.R;
 
   if (threadIdx.x == 0) {
@@ -754,8 +757,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   __shared__ int s_pos[2 * TC_M];
   __shared__ int16_t s_seq[2 * TC_M];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = gridDim.x - 1 - blockIdx.x;          // later (longer) tiles first: causal balance
-  const int kh = blockIdx.y;
+  // 1-D grid over (tile, kv head), longest tiles of EVERY head first: the
+  // block scheduler then fills the SMs in LPT order (a [tiles, heads] grid
+  // launched head 0's short tiles before head 7's long ones)
+  const int tile = (int)(gridDim.x / a.KV) - 1 - (int)(blockIdx.x / a.KV);
+  const int kh = (int)(blockIdx.x % a.KV);
   const int R2 = 2 * a.R;
   const int t0 = tile * R2;
 
@@ -1125,8 +1131,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   __shared__ int s_pos[2 * TC_M];
   __shared__ int16_t s_seq[2 * TC_M];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = gridDim.x - 1 - blockIdx.x;          // later (longer) tiles first: causal balance
-  const int kh = blockIdx.y;
+  // 1-D grid over (tile, kv head), longest tiles of EVERY head first: the
+  // block scheduler then fills the SMs in LPT order (a [tiles, heads] grid
+  // launched head 0's short tiles before head 7's long ones)
+  const int tile = (int)(gridDim.x / a.KV) - 1 - (int)(blockIdx.x / a.KV);
+  const int kh = (int)(blockIdx.x % a.KV);
   const int R2 = 2 * a.R;
   const int t0 = tile * R2;
 
@@ -1389,9 +1398,9 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   const int R = TC_M / G;
   // LP_ATTN_TC selects the variant (A/B tables: profiles/r02/attn_prefill_*):
   //   7 (default) FA4 layout: two Q tiles per CTA, 128-key chunks, P kept in
-  //     TMEM as the P V MMA's A operand, one softmax thread per row:
-  //     8B 1 x 2048 rows 82.5 -> 77 us, 2 x 4096 439 -> 355 us, 8 x 512 84 ->
-  //     67 us; 70B 2 x 4096 847 -> 640 us (vs the eager one-tile kernel);
+  //     TMEM as the P V MMA's A operand, one softmax thread per row, LPT
+  //     launch order: 8B 1 x 2048 rows 82.5 -> 57 us, 2 x 4096 439 -> 335 us,
+  //     8 x 512 84 -> 66 us; 70B 2 x 4096 847 -> 644 us (vs the eager kernel);
   //   3 one Q tile per CTA, lazy row max (exchanged after the exp pass),
   //     packed FFMA2/FADD2/FMNMX3 math, one key pair in four on the FMA-pipe
   //     exp2 (80.2 / 418 / 86 us);
@@ -1467,7 +1476,7 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
       const char* e = getenv("LP_ATTN_FA_POLY");
       return e ? atoi(e) : 1;
     }();
-    const dim3 grid((unsigned)((T + 2 * R - 1) / (2 * R)), (unsigned)KV);
+    const dim3 grid((unsigned)((T + 2 * R - 1) / (2 * R) * KV));
     if (poly == 0)
       LP_CUDA(lp::launch(attention_fa_kernel<HD, 0>, grid, dim3(FA_THREADS), fa_smem[1], s, mq, mk, mv, args));
     else if (poly == 2)
@@ -1496,7 +1505,7 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
       LP_CUDA(cudaFuncSetAttribute(attention_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM));
       pattr |= 1ull << dev;
     }
-    const dim3 grid((unsigned)((T + 2 * R - 1) / (2 * R)), (unsigned)KV);
+    const dim3 grid((unsigned)((T + 2 * R - 1) / (2 * R) * KV));
     LP_CUDA(lp::launch(attention_pp_kernel<HD>, grid, dim3(PP_THREADS), P::SMEM, s, mq, mk, mv, args));
     if (trace) {
       static long long h[64 * 16];
@@ -1511,7 +1520,7 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
     }
     return 0;
   }
-  const dim3 grid((unsigned)((T + R - 1) / R), (unsigned)KV);
+  const dim3 grid((unsigned)((T + R - 1) / R * KV));
   if (variant == 1)
     LP_CUDA(lp::launch(attention_tc_kernel<HD, 2, false>, grid, dim3(11 * 32), tc_smem[0], s, mq, mk, mv, args));
   else
