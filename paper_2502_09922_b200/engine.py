@@ -57,6 +57,11 @@ def device_view(ptr: int, nbytes: int, device: int, dtype=None, shape=None):
     return t.view(shape) if shape is not None else t
 
 
+# copy-engine streams per node for the hybrid executor's pinned-host DMA (its
+# blocks alternate between them); LP_HOST_DMA_STREAMS overrides
+HOST_DMA_STREAMS = int(os.environ.get("LP_HOST_DMA_STREAMS", "1"))
+
+
 class MulticastEngine:
     """One compiled λPipe multicast over a fixed block table."""
 
@@ -585,9 +590,10 @@ class Cluster:
         for node in self.exec_nodes:
             k_ops, d_ops = self.engine.node_ops(node)
             if d_ops:
-                (st,) = self.ce_streams(node, 1)
-                st.wait_event(start)
-                self.engine.run_host_dma(node, epoch, [st.cuda_stream])
+                sts = self.ce_streams(node, HOST_DMA_STREAMS)
+                for st in sts:
+                    st.wait_event(start)
+                self.engine.run_host_dma(node, epoch, [st.cuda_stream for st in sts])
             if k_ops:
                 run_kernel.append(node)
         if run_kernel:
