@@ -331,6 +331,14 @@ HYBRID_TILE = 64 << 20   # DMA tile of the PCIe hop = relay granule of the kerne
 SPLIT_CE_TILE = 64 << 20  # copy-engine blocks of the split executor
 
 
+def split_tiles(n_blocks: int, kernel_tile: int, ce_split: int = 2) -> list:
+    """Per-block tile sizes of the split executor (lp_mc_create_tiled): the
+    copy-engine blocks (b % ce_split == 0, the engine's option) in
+    SPLIT_CE_TILE tiles (few stream ops), the in-kernel ones in kernel_tile
+    (a tile is one CTA's unit)."""
+    return [SPLIT_CE_TILE if b % ce_split == 0 else kernel_tile for b in range(n_blocks)]
+
+
 def choose_strategy(host_source: bool, n_gpus: int) -> str:
     """Full-replica scale-out from the box's shared host copy with >= 2 GPUs:
     sharded PCIe loads + NVLink exchange (2.0x the binomial tree's host
@@ -382,10 +390,7 @@ class ScaleOut:
             executor, tile_bytes = choose_executor(plan, tile_bytes)
         lay = plan.layout
         if executor == "split" and not isinstance(tile_bytes, (list, tuple)):
-            # per-executor tiling: the copy-engine blocks (b % 2 == 0) in
-            # SPLIT_CE_TILE tiles (few stream ops), the in-kernel ones in
-            # tile_bytes (a tile is one CTA's unit)
-            tile_bytes = [SPLIT_CE_TILE if b % 2 == 0 else tile_bytes for b in range(len(lay.block_offsets))]
+            tile_bytes = split_tiles(len(lay.block_offsets), tile_bytes)
         if distributed:
             self.cluster = E.Cluster.distributed(lay.block_offsets, lay.block_lengths, lay.weights_bytes,
                                                  host_node=plan.host_source, tile_bytes=tile_bytes)

@@ -265,6 +265,20 @@ class Server:
             r.unit, r.slot, r.kv_len, r.needs_prefill = u.uid, s, 0, True
             u.busy[s] = r
 
+    def _pipeline_pass(self, reqs: list) -> list:
+        """The requests one pipeline pass runs: every decode, and prefills in
+        slot order while they fit ``pipeline_prefill_tokens`` (always at
+        least one, so a long prompt still makes progress)."""
+        keep, n_pf = [], 0
+        for r in reqs:
+            if r.needs_prefill:
+                n = len(r.prompt) + len(r.out)
+                if n_pf and n_pf + n > self.pipeline_prefill_tokens:
+                    continue
+                n_pf += n
+            keep.append(r)
+        return keep
+
     def _mode_switch(self, now):
         switched_nodes = []
         for u in sorted(self.units.values(), key=lambda x: x.uid):
@@ -375,15 +389,7 @@ class Server:
             if not reqs:
                 return out
         if u.kind == "pipeline":
-            keep, n_pf = [], 0
-            for r in reqs:
-                if r.needs_prefill:
-                    n = len(r.prompt) + len(r.out)
-                    if n_pf and n_pf + n > self.pipeline_prefill_tokens:
-                        continue
-                    n_pf += n
-                keep.append(r)
-            reqs = keep
+            reqs = self._pipeline_pass(reqs)
         tokens, pos, seq, last = [], [], [], []
         for r in reqs:
             if r.needs_prefill:

@@ -112,3 +112,26 @@ def test_pipeline_prefill_budget():
     assert Server.prefill_budget(I.build_layout(I.CONFIGS["llama3-8b"], 16), 64) == 64
     src = inspect.getsource(A.AutoscaleServer.__init__)
     assert "pipeline_prefill_tokens" in src and "pipeline_batch" in src
+
+
+def test_pipeline_pass_prefill_budget():
+    """A pipeline pass runs every decode and prefills in slot order while they
+    fit the token budget, at least one (Server._pipeline_pass)."""
+    from types import SimpleNamespace
+    from paper_2502_09922_b200.serving import Server
+
+    def req(n, prefill):
+        return SimpleNamespace(prompt=[0] * n, out=[], needs_prefill=prefill)
+    srv = SimpleNamespace(pipeline_prefill_tokens=300)
+    reqs = [req(128, True), req(128, True), req(10, False), req(128, True), req(40, True)]
+    got = Server._pipeline_pass(srv, reqs)
+    assert got == [reqs[0], reqs[1], reqs[2], reqs[4]]       # 128 + 128 + 40 <= 300; the third 128 waits
+    srv.pipeline_prefill_tokens = 64
+    got = Server._pipeline_pass(srv, [req(500, True), req(10, True), req(1, False)])
+    assert [len(r.prompt) for r in got] == [500, 1]           # one over-budget prompt still runs alone
+
+
+def test_split_executor_tiles():
+    from paper_2502_09922_b200 import scaleout as SO
+    t = SO.split_tiles(5, 2 << 20)
+    assert t == [SO.SPLIT_CE_TILE, 2 << 20, SO.SPLIT_CE_TILE, 2 << 20, SO.SPLIT_CE_TILE]
