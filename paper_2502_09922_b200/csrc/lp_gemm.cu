@@ -899,6 +899,37 @@ int dispatch(const void* W, const void* W2, int64_t N, int64_t K, const void* X,
       bt128 = (e && e[0] == '1') ? 1 : 0;
     }
     if (bt128) return launch<128, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
+    // the non-linear epilogue cannot take the stream-K tail: when 256-row x
+    // 256-token pair tiles leave a partial last wave, the rows that would
+    // fill it go to a second launch in 64-token tiles (a quarter-size round
+    // instead of a full one; T = 2048 / 1024: 448 / 224 pair tiles = 6.05 /
+    // 3.03 waves of 74).  LP_SWIGLU_TAIL=0 keeps one launch.
+    static int tail_env = -1;
+    static int sms = 0;
+    if (tail_env < 0) {
+      const char* e = getenv("LP_SWIGLU_TAIL");
+      tail_env = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (!sms) {
+      int dev = 0;
+      LP_CUDA(cudaGetDevice(&dev));
+      LP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (tail_env && sms >= 2) {
+      const int64_t slots = sms / 2;
+      const int64_t tt = (T + 255) / 256, n2 = (N + 255) / 256, total = n2 * tt;
+      const int64_t rounds = (total + slots - 1) / slots;
+      const int64_t n_main2 = rounds >= 2 ? (rounds - 1) * slots / tt : 0;
+      const int64_t n_tail2 = n2 - n_main2;
+      if (n_main2 >= 1 && n_tail2 >= 1 && n_tail2 * ((T + 63) / 64) <= slots) {
+        const int64_t n_main = n_main2 * 256;
+        const int r = launch<256, EPI>(W, W2, n_main, K, X, T, out, ldo, split_k, s);
+        if (r) return r;
+        const size_t off = (size_t)n_main * (size_t)K * 2;
+        return launch<64, EPI>((const char*)W + off, (const char*)W2 + off, N - n_main, K, X, T,
+                               (__nv_bfloat16*)out + n_main, ldo, split_k, s);
+      }
+    }
   }
   return launch<256, EPI>(W, W2, N, K, X, T, out, ldo, split_k, s);
 }

@@ -58,7 +58,10 @@ def test_gemm_matches_fp32(n, k, t, epi, split):
 
 
 @pytest.mark.parametrize("n,k,t", [(688, 256, 24), (1536, 512, 1), (640, 1024, 130), (1408, 512, 600),
-                                   (384, 4096, 257)])
+                                   (384, 4096, 257),
+                                   # > 1 wave of 256 x 256 pair tiles: the partial last wave's rows go
+                                   # to a 64-token-tile launch (224 tiles; ragged 90 tiles at T = 1100)
+                                   (14336, 256, 1024), (4608, 128, 1100)])
 def test_gemm_swiglu_matches_fp32(n, k, t):
     import torch
     g = torch.Generator(device="cuda").manual_seed(n + k)
