@@ -1151,17 +1151,30 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     }
     lp::mbar_init(&o_final, 1);
     lp::fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+    // Q and the first K / V chunk (chunk 0 of the tile's first sequence)
+    // go out before the token table and the CTA barrier: the first S MMA's
+    // operand latency overlaps the rest of the prologue
+    lp::pdl_wait();
+    lp::mbar_expect_tx(&q_full, 2 * C::Q_BYTES);
+    for (int t = 0; t < 2; ++t)
+      for (int at = 0; at < C::ATOMS; ++at)
+        tma3d(sm + C::OFF_Q + t * C::Q_BYTES + at * ATOM, &tmQ, &q_full, at * 64, kh * a.G, t0 + t * a.R);
+    const int row0 = a.seq[t0] * a.KV + kh;
+    lp::mbar_expect_tx(&k_full[0], C::KV_BYTES);
+    lp::mbar_expect_tx(&v_full[0], C::KV_BYTES);
+    for (int at = 0; at < C::ATOMS; ++at) {
+      tma3d(sm + C::OFF_K + at * (TC_KEYS * 128), &tmK, &k_full[0], at * 64, 0, row0);
+      tma3d(sm + C::OFF_V + at * (TC_KEYS * 128), &tmV, &v_full[0], at * 64, 0, row0);
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      lp::smem_u32(&tmem_base)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmQ) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmK) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
   }
   lp::pdl_wait();
   lp::pdl_trigger();
@@ -1183,13 +1196,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 
   if (warp == 0 || warp == 10) {
     if (lane == 0) {
-      const bool is_k = warp == 0;
-      if (is_k) {
-        lp::mbar_expect_tx(&q_full, 2 * C::Q_BYTES);
-        for (int t = 0; t < 2; ++t)
-          for (int at = 0; at < C::ATOMS; ++at)
-            tma3d(sm + C::OFF_Q + t * C::Q_BYTES + at * ATOM, &tmQ, &q_full, at * 64, kh * a.G, t0 + t * a.R);
-      }
+      const bool is_k = warp == 0;     // Q, K(0) and V(0) were issued in the prologue
       uint64_t* full = is_k ? k_full : v_full;
       uint64_t* empty = is_k ? k_empty : v_empty;
       const CUtensorMap* map = is_k ? &tmK : &tmV;
@@ -1199,6 +1206,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         run(lo, hi, sq, nch);
         const int row = sq * a.KV + kh;
         for (int c = 0; c < nch; ++c, ++it) {
+          if (it == 0) continue;
           const int st = it & 1;
           if (it >= 2) lp::mbar_wait(&empty[st], ((it >> 1) - 1) & 1);
           lp::mbar_expect_tx(&full[st], C::KV_BYTES);
