@@ -26,10 +26,10 @@
 // more than 2^8 (P then stays <= 256, exact enough in fp16; the row sum l
 // uses the same m), so O almost never needs rescaling: when it does, the
 // row's softmax threads rescale it in TMEM (after the previous P V) before
-// releasing P_j.  Final: O / l.  The default (lazy) variant computes P_j with
-// the current m first and only then combines the halves' raw maxima (one
-// atomicMax slot + a 64-thread named barrier per chunk), recomputing P_j from
-// the S values still in registers when m has to move.
+// releasing P_j.  Final: O / l.  Its lazy variant (LP_ATTN_TC=3) computes
+// P_j with the current m first and only then combines the halves' raw maxima
+// (one atomicMax slot + a 64-thread named barrier per chunk), recomputing P_j
+// from the S values still in registers when m has to move.
 //
 //   warp 0   : TMA producer (Q once, then K chunks)      warp 10: TMA (V chunks)
 //   warp 1   : TMEM allocator + MMA issuer (one thread)
