@@ -42,7 +42,9 @@ def _max(x: float) -> float:
 
 
 def run_engine(plan, executor, iters, tile):
-    so = SO.ScaleOut(plan, distributed=True, executor=executor, tile_bytes=tile,
+    # the bench's in-kernel configuration: receivers pull with LDG vectors
+    # (copy_mode 0), 64 CTAs per receiver
+    so = SO.ScaleOut(plan, distributed=True, executor=executor, tile_bytes=tile, copy_mode=0, pull_ctas=64,
                      device=torch.cuda.current_device())
     so.load_sources()
     times = []
@@ -140,8 +142,8 @@ def main():
         arms.append((strat, baseline_schedule(strat, plan.nodes, plan.layout.plan, cluster)))
     for name, sched in arms:
         p = dataclasses.replace(plan, schedule=sched)
-        execs = [("kernel", E.DEFAULT_TILE), ("ce", SO.CE_TILE)] if name != "broadcast_groups" \
-            else [("kernel", E.DEFAULT_TILE)]
+        execs = [("kernel", 2 << 20), ("ce", SO.CE_TILE)] if name != "broadcast_groups" \
+            else [("kernel", 2 << 20)]
         for ex, tile in execs:
             med, best, ok = run_engine(p, ex, a.iters, tile)
             emit(f"{name}/{ex}", med, best, ok, sched.step_count)
