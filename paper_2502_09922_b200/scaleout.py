@@ -326,6 +326,7 @@ def node_ops(plan: ScaleOutPlan, node: int, direction: int = 1) -> list:
     return out
 
 
+KERNEL_TILE = 2 << 20    # in-kernel executor (a tile is one CTA's unit): measured best on 8B / 13B images
 CE_TILE = 256 << 20
 HYBRID_TILE = 64 << 20   # DMA tile of the PCIe hop = relay granule of the kernel
 SPLIT_CE_TILE = 64 << 20  # copy-engine blocks of the split executor
@@ -348,7 +349,7 @@ def choose_strategy(host_source: bool, n_gpus: int) -> str:
     return "sharded_host" if host_source and n_gpus >= 2 else "lambda"
 
 
-def choose_executor(plan: ScaleOutPlan, tile_bytes: int = E.DEFAULT_TILE):
+def choose_executor(plan: ScaleOutPlan, tile_bytes: int = KERNEL_TILE):
     """Measured policy (profiles/mc_sweeps_r01.md, p2p_micro_r01.txt):
     host-sourced schedules run hybrid — the PCIe hop as pinned DMA on the
     copy engines (55.3 GB/s vs 51.4 GB/s for SM-issued PCIe reads), NVLink
@@ -540,7 +541,7 @@ class TieredScaleOut:
     takes: its pipelines include the warm pipeline."""
 
     def __init__(self, tp: TieredPlan, node_devices: dict | None = None, seed: int = 0,
-                 tile_bytes: int = 1 << 20, config=None, block_count: int | None = None):
+                 tile_bytes: int = KERNEL_TILE, config=None, block_count: int | None = None):
         self.tp = tp
         self.seed = seed
         self.dev_of = dict(node_devices or {})
