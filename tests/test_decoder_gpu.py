@@ -279,3 +279,20 @@ def test_prefill_attention_tcgen05_causal(hd, H, KV, lens, cap):
         err = (out[row:row + n].float() - ref).abs().max().item()
         assert err < 2e-2, (s, n, err)
         row += n
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_prefill_attention_random_ragged_batches(seed):
+    """Random ragged prompt batches (1-6 prompts of 1-700 tokens, GQA groups
+    of 1-8 heads, head_dim 64 / 128) through whichever prefill kernel the
+    dispatch picks (tcgen05 FA layout for GQA >= 4 or caches > 256 keys,
+    mma.sync otherwise), vs a torch fp32 causal softmax."""
+    import random
+    rnd = random.Random(1000 + seed)
+    hd = rnd.choice([64, 128])
+    KV = rnd.choice([2, 4, 8])
+    G = rnd.choice([1, 2, 4, 8])
+    lens = [rnd.randint(1, 700) for _ in range(rnd.randint(1, 6))]
+    while sum(lens) * KV < 1024:          # the prefill (many-row) path
+        lens.append(rnd.randint(64, 700))
+    test_prefill_attention_tcgen05_causal(hd, G * KV, KV, lens, 0)
