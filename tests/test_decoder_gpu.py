@@ -296,3 +296,18 @@ def test_prefill_attention_random_ragged_batches(seed):
     while sum(lens) * KV < 1024:          # the prefill (many-row) path
         lens.append(rnd.randint(64, 700))
     test_prefill_attention_tcgen05_causal(hd, G * KV, KV, lens, 0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gemm_random_shapes(seed):
+    """Random prefill / decode shapes through the residual-add GEMM (split-K,
+    CTA pairs, the stream-K tail) and the fused SwiGLU (incl. its tail
+    launch), vs torch fp32."""
+    import random
+    rnd = random.Random(2000 + seed)
+    n = 128 * rnd.randint(1, 96) + rnd.choice([0, 0, 16, 48])
+    k = 64 * rnd.randint(1, 48)
+    t = rnd.choice([rnd.randint(1, 64), rnd.randint(65, 700), rnd.randint(700, 2500)])
+    test_gemm_matches_fp32(n, k, t, 0, 1)
+    if k % 64 == 0:
+        test_gemm_swiglu_matches_fp32(n, k, t)
