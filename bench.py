@@ -483,6 +483,9 @@ def main():
                          if int(ln.split(",")[1]) == 0)
         gpu_source = {"workload": f"{C2_MODEL} bf16 GPU0->{N - 1} peers, b={C2_MC_BLOCKS}, k=1",
                       "schedule_ceiling": round(M2 / src_egress, 4), "executors": {}}
+        # in-kernel: 64 pull CTAs per receiver (96 CTAs / window 6 measured
+        # 0.698 vs 0.673 without verify, but no better beside the verify
+        # kernels: profiles/r02/mc_gpu_source_n4_ctas.txt)
         for name, kw in (("kernel", dict(executor="kernel", tile_bytes=2 << 20, pull_ctas=64, copy_mode=0)),
                          ("copy_engine", dict(executor="ce", tile_bytes=SO.CE_TILE))):
             so2 = SO.ScaleOut(plan2, distributed=True, push_ctas=0, seed=SEED, device=dev, direction=1,

@@ -383,7 +383,7 @@ class ScaleOut:
     def __init__(self, plan: ScaleOutPlan, distributed: bool = False, tile_bytes: int = E.DEFAULT_TILE,
                  push_ctas: int = 0, pull_ctas: int = 64, seed: int = 0, device: int = 0, direction: int = 1,
                  copy_mode: int = 1, chunk_bytes: int = 16384, executor: str = "kernel", ce_streams: int = 1,
-                 verify: bool = False, verify_ctas: int | None = None):
+                 verify: bool = False, verify_ctas: int | None = None, window: int = 3):
         self.plan = plan
         self.distributed = distributed
         self.push_ctas, self.pull_ctas = push_ctas, pull_ctas
@@ -408,7 +408,7 @@ class ScaleOut:
             executor = "hybrid"
         self.executor = executor
         self.ce_streams = ce_streams
-        self.cluster.engine.configure(direction, copy_mode, copy_mode, chunk_bytes, 3)
+        self.cluster.engine.configure(direction, copy_mode, copy_mode, chunk_bytes, window)
         self.cluster.engine.set_option("host_dma", int(executor == "hybrid"))
         self.cluster.engine.set_option("ce_split", 2 if self.split else 0)
         self.kernel_launches = 0      # multicast kernels of the last run (this process)
