@@ -205,7 +205,7 @@ int lp_rope_kv(const float* qkv, int64_t T, int n_heads, int n_kv, int head_dim,
 /* ragged causal GQA attention: token t attends to 0..pos[t] of seq[t]; k
  * cache bf16, v cache fp16 (lp_rope_kv), out bf16.  head_dim 32..128
  * (multiple of 32), H/KV <= 8.  T*KV >= 1024 (prefill), head_dim 64/128,
- * max_len > 256 or H/KV >= 4:
+ * max_len > 160 or H/KV >= 4:
  * tcgen05/TMEM kernel (128-row tiles of R tokens x H/KV heads, TMA-fed,
  * two tiles per CTA, fp32 S and O in TMEM, fp16 P kept in TMEM as the P.V
  * MMA's A operand; LP_ATTN_TC selects the other variants, 0 = mma.sync);

@@ -1417,10 +1417,15 @@ int launch_tc(const void* q, const void* k_cache, const void* v_cache, const int
   //   with 0 / 2 of 4 key pairs on the FMA pipe: attn_prefill_lazy_ab.txt)
   //   2 the 64-key ping-pong kernel (P in smem; its N = 64 S MMAs are
   //     smem-bound).
-  static const int variant = [] {
+  static const int variant_env = [] {
     const char* e = getenv("LP_ATTN_TC");
     return e ? atoi(e) : 7;
   }();
+  // groups of <= 2 heads (R >= 64 tokens per tile) with short caches: the FA
+  // kernel's 2R-token CTAs would span several prompts (each walking the
+  // others' chunks masked), so the one-tile kernel runs them (MHA 16 x 128
+  // tokens: 78 vs 103 us, profiles/r02/attn_prefill_mha_short.txt)
+  const int variant = (variant_env == 7 && G <= 2 && max_len <= 512) ? 1 : variant_env;
   const uint32_t kbox = variant == 2 ? PP_KEYS : TC_KEYS;   // 7 and the one-tile kernels: 128-key chunks
   CUtensorMap mq, mk, mv;
   const uint64_t rows = (uint64_t)1 << 24;   // sequence x kv-head rows of the caches (unbounded here)

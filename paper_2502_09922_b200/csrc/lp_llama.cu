@@ -1043,14 +1043,14 @@ int lp_attention(const void* q, const void* k_cache, const void* v_cache, const 
       const char* e = getenv("LP_ATTN_TC");
       return e ? atoi(e) : 1;
     }();
-    // short caches of MHA models stay on the mma.sync kernel (13B-shaped 16 x
-    // 128-token prompts: 81 vs 106 us on tcgen05, whose 2 x 128-token tiles
-    // then span several prompts); GQA groups of >= 4 heads take tcgen05 at any
-    // length (8B 29.3 -> 27.3 us, 70B 51.4 -> 44.7 us,
-    // profiles/r02/attn_prefill_short_ab.txt)
+    // caches of at most ~one 128-key chunk of MHA models stay on the mma.sync
+    // kernel (16 x 128-token prompts: 76 vs 78 us); longer ones take tcgen05
+    // (16 x 200: 365 -> 148 us for 13B heads); GQA groups of >= 4 heads take
+    // tcgen05 at any length (8B 29.3 -> 27.3 us, 70B 51.4 -> 44.7 us,
+    // profiles/r02/attn_prefill_short_ab.txt, attn_prefill_mha_short.txt)
     static const int64_t tc_min_len = [] {   // LP_ATTN_TC_MIN_LEN: caches longer than this take tcgen05
       const char* e = getenv("LP_ATTN_TC_MIN_LEN");
-      return e ? (int64_t)atoll(e) : (int64_t)256;
+      return e ? (int64_t)atoll(e) : (int64_t)160;
     }();
     if (tc_env && (max_len > tc_min_len || n_heads / n_kv >= 4)) {
       const int r = lp::attention_tc(q, k_cache, v_cache, pos, seq, T, n_heads, n_kv, head_dim, max_len, scale,
